@@ -1,0 +1,155 @@
+/*
+ * dct16a.h — C ABI of the B200-native batched 16x16 approximate-DCT path of
+ * arXiv 1606.05562 ("A multiplierless 16-point DCT approximation", the matrix T
+ * of PAPER.md:270-287, evaluated with the 60-addition factorisation
+ * T = P2·M4·M3·M2·P1·M1 of Eq. (1)).
+ *
+ * Every entry point is asynchronous on the given CUDA stream (`stream` is a
+ * cudaStream_t passed as void*; NULL = legacy default stream).  All data
+ * pointers are DEVICE pointers unless the name says `host`.  The caller owns
+ * and frees every buffer; the library never allocates device memory, never
+ * synchronises the stream and keeps no per-call state (constants live in
+ * __constant__ memory).  Calls are thread-safe and re-entrant.
+ *
+ * Errors: every function validates all arguments synchronously before any
+ * launch and returns 0 on success or a negative DCT16A_E* code, leaving the
+ * outputs untouched on a validation error.  dct16a_last_error() returns a
+ * thread-local message for the last failure of the calling thread.  Device
+ * faults surface at the caller's next synchronisation.
+ *
+ * Pixels: bit_depth 8 -> uint8 samples; bit_depth 10 -> int16 samples that
+ * MUST lie in [0, 1023] (values outside give undefined coefficients: the
+ * kernels use 16-bit SWAR lanes sized for that range).
+ *
+ * Blocks: each image is cut into disjoint 16x16 blocks A_k in row-major block
+ * order (all blocks, reading A3 of DESIGN.md).  Block
+ * (n, by, bx) has linear index b = (n·BY + by)·BX + bx with BY = height/16 and
+ * BX = width/16.
+ *
+ * Coefficients: Z = T·X·Tᵀ per block (PAPER.md:870-880 with the scale S
+ * absorbed into quantisation; k = row = vertical frequency,
+ * reading A5), stored block-major int32: coef[b·256 + 16·k + l] (reading A17).
+ * The pitch applies to the image side only.
+ */
+#ifndef DCT16A_H
+#define DCT16A_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define DCT16A_API __attribute__((visibility("default")))
+#else
+#define DCT16A_API
+#endif
+
+/* ---- return codes ------------------------------------------------------ */
+#define DCT16A_OK        0
+#define DCT16A_ENULL    -1  /* a required pointer is NULL                         */
+#define DCT16A_ESHAPE   -2  /* width/height not positive multiples of 16, batch<1,
+                               valid_height outside (0, height]                   */
+#define DCT16A_EPITCH   -3  /* pitch < width·elem, pitch or image stride not a
+                               multiple of 16, image stride < pitch·height (batch>1) */
+#define DCT16A_EALIGN   -4  /* a device pointer is not 16-byte aligned (TMA)      */
+#define DCT16A_EDOMAIN  -5  /* r outside [1,256], step < 1, unknown mode,
+                               bit_depth not 8 or 10, r range empty               */
+#define DCT16A_ECUDA    -6  /* kernel launch, copy or tensor-map encode failed    */
+
+/* ---- image batch descriptor -------------------------------------------- */
+typedef struct dct16a_desc {
+    int32_t width;          /* pixels per row, multiple of 16                     */
+    int32_t height;         /* rows per image, multiple of 16                     */
+    int32_t valid_height;   /* rows counted by SSE/PSNR, 0 < valid_height <= height
+                               (1080 for 1088-padded frames, reading A13)         */
+    int32_t batch;          /* number of images / frames                          */
+    int32_t bit_depth;      /* 8 (uint8) or 10 (int16 in [0,1023])                */
+    int32_t reserved;       /* must be 0                                          */
+    int64_t pitch_bytes;    /* bytes between rows, multiple of 16                 */
+    int64_t image_stride_bytes; /* bytes between images, multiple of 16           */
+} dct16a_desc;
+
+/* ---- quantiser parameters (S folded in) -------------- */
+#define DCT16A_ZONAL    0   /* keep the first r zig-zag coefficients */
+#define DCT16A_UNIFORM  1   /* q = sign(B)·floor(|B|/step + 1/2), B = Z/sqrt(g_k·g_l)
+                               (reading A9; decided exactly in integers)           */
+typedef struct dct16a_quant {
+    int32_t mode;           /* DCT16A_ZONAL or DCT16A_UNIFORM                     */
+    int32_t r;              /* zonal: retained coefficients, 1..256               */
+    int32_t step;           /* uniform: integer step Δ >= 1                       */
+    int32_t reserved;       /* must be 0                                          */
+} dct16a_quant;
+
+/*
+ * dct16a_forward — Z = T·X·Tᵀ for every block (separable
+ * row/column passes of the Eq. (1) network as in PAPER.md:1072-1090).
+ *   src  : image batch laid out as described by *desc (uint8 or int16).
+ *   coef : int32 output, batch·BY·BX·256 entries, block-major (see above).
+ * Integer-exact.  |Z| <= 65280 (8-bit) / 261888 (10-bit).
+ */
+DCT16A_API int dct16a_forward(const void* src, const dct16a_desc* desc,
+                              int32_t* coef, void* stream);
+
+/*
+ * dct16a_quantize — the quantisation stage with S folded in.
+ *   coef   : int32 block-major Z as written by dct16a_forward.
+ *   qcoef  : int32 out, same shape.  Zonal: Z ⊙ M_r (M_r = first r zig-zag
+ *            positions, reading A4).  Uniform: the integer
+ *            levels q (exact decision, ties away from zero).
+ *   scaled : optional float32 out (may be NULL), same shape.  Zonal:
+ *            s_k·s_l·(Z ⊙ M_r) = B′ of PAPER.md:874-894.  Uniform: s_k·s_l·Z = B.
+ *            Here s = diag(S) of PAPER.md:315-329.
+ */
+DCT16A_API int dct16a_quantize(const int32_t* coef, const dct16a_desc* desc,
+                               const dct16a_quant* quant, int32_t* qcoef,
+                               float* scaled, void* stream);
+
+/*
+ * dct16a_inverse — A′ = Ĉᵀ·B′·Ĉ, rounded half away from
+ * zero and clamped to [0, 2^b - 1] (reading A6), written as pixels.
+ *   qcoef : int32 levels from dct16a_quantize (zonal: Z ⊙ M_r; uniform: q).
+ *   recon : pixels in the layout, pitch and type of *desc.
+ * Zonal reconstruction is exact: N = Tᵀ·(W ⊙ qcoef)·T with W = 2304/(g_k·g_l)
+ * and pixel = round(N/2304) decided on the integer N.  Uniform reconstruction
+ * evaluates Tᵀ·(Δ·q·s_k·s_l)·T in float64 (reading A10).
+ */
+DCT16A_API int dct16a_inverse(const int32_t* qcoef, const dct16a_desc* desc,
+                              const dct16a_quant* quant, void* recon, void* stream);
+
+/*
+ * dct16a_psnr — per-image SSE over the first valid_height rows and
+ * PSNR = 10·log10(peak²·P/SSE), peak = 2^b - 1, P = valid_height·width,
+ * +INFINITY when SSE = 0 (readings A7/A13).
+ *   ref, test : two image batches with the same *desc.
+ *   sse       : uint64 out [batch] (exact).
+ *   psnr      : optional float64 out [batch] (may be NULL).
+ */
+DCT16A_API int dct16a_psnr(const void* ref, const void* test, const dct16a_desc* desc,
+                           uint64_t* sse, double* psnr, void* stream);
+
+/*
+ * dct16a_codec — the fused path forward -> quantise -> inverse -> SSE/PSNR
+ * in one pass over the input.  Results are identical,
+ * byte for byte, to dct16a_forward -> dct16a_quantize -> dct16a_inverse ->
+ * dct16a_psnr.
+ *   recon : optional pixels out (may be NULL: nothing is written).
+ *   sse   : uint64 out [batch] (exact; overwritten, not accumulated).
+ *   psnr  : optional float64 out [batch] (may be NULL).
+ */
+DCT16A_API int dct16a_codec(const void* src, const dct16a_desc* desc,
+                            const dct16a_quant* quant, void* recon,
+                            uint64_t* sse, double* psnr, void* stream);
+
+/* Thread-local description of the calling thread's last failure ("" if none). */
+DCT16A_API const char* dct16a_last_error(void);
+
+/* Library version and build target, e.g. "dct16a 0.1.0 sm_100a". */
+DCT16A_API const char* dct16a_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DCT16A_H */

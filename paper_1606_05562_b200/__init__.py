@@ -1,0 +1,81 @@
+"""paper_1606_05562_b200 — B200-native batched 16x16 approximate DCT of
+arXiv 1606.05562 (multiplierless 16-point DCT approximation T, 60 additions).
+
+The compute lives in libdct16a.so (hand-written sm_100a CUDA behind the C ABI
+of include/dct16a.h); this package is the thin Python binding (``_lib``, same
+names as the C entry points) plus allocation helpers.  PyTorch provides device
+memory, streams and process groups only.
+"""
+from __future__ import annotations
+
+from ._lib import (UNIFORM, ZONAL, Dct16aError, Desc, Quant, dct16a_codec, dct16a_forward,  # noqa: F401
+                   dct16a_inverse, dct16a_last_error, dct16a_psnr, dct16a_quantize, dct16a_version,
+                   desc_of, lib, make_desc, make_quant)
+
+__version__ = "0.1.0"
+
+
+def forward(images, out=None, stream=None):
+    """Z = T·X·Tᵀ for every 16x16 block of a (batch, H, W) uint8/int16 CUDA
+    tensor; returns int32 (batch·H/16·W/16, 16, 16) block-major coefficients."""
+    import torch
+    if images.dim() == 2:
+        images = images.unsqueeze(0)
+    n, h, w = images.shape
+    if out is None:
+        out = torch.empty((n * (h // 16) * (w // 16), 16, 16), dtype=torch.int32, device=images.device)
+    dct16a_forward(images, out, desc_of(images), stream)
+    return out
+
+
+def codec(images, mode="zonal", r=16, step=16, valid_height=None, want_recon=True, stream=None):
+    """Fused forward -> quantise (S folded) -> inverse -> reconstruct -> SSE/PSNR.
+    Returns (recon or None, sse int64[batch], psnr float64[batch])."""
+    import torch
+    if images.dim() == 2:
+        images = images.unsqueeze(0)
+    d = desc_of(images, valid_height=valid_height)
+    n = images.shape[0]
+    sse = torch.empty(n, dtype=torch.int64, device=images.device)
+    psnr = torch.empty(n, dtype=torch.float64, device=images.device)
+    recon = torch.empty_like(images) if want_recon else None
+    dct16a_codec(images, make_quant(mode, r, step), sse, recon, psnr, d, stream)
+    return recon, sse, psnr
+
+
+def forward_host(host_images, host_coef, chunk_images=256, device=None, bufs=None):
+    """End-to-end forward transform from PINNED host images to PINNED host
+    coefficients: the batch is cut into chunks; chunk i's host->device copy,
+    transform and device->host copy run on stream i % 2, so copies in both
+    directions overlap each other and the transform.  Returns the device
+    buffers for reuse (pass them back as `bufs`).
+
+    host_images: (batch, H, W) uint8/int16 pinned CPU tensor.
+    host_coef:   (batch·H/16·W/16, 16, 16) int32 pinned CPU tensor.
+    """
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    n, h, w = host_images.shape
+    per_img = (h // 16) * (w // 16)
+    c = max(1, min(chunk_images, n))
+    if bufs is None:
+        streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+        xin = [torch.empty((c, h, w), dtype=host_images.dtype, device=dev) for _ in range(2)]
+        cout = [torch.empty((c * per_img, 16, 16), dtype=torch.int32, device=dev) for _ in range(2)]
+        bufs = (streams, xin, cout)
+    streams, xin, cout = bufs
+    cur = torch.cuda.current_stream(dev)
+    for s in streams:
+        s.wait_stream(cur)
+    for i, s0 in enumerate(range(0, n, c)):
+        m = min(c, n - s0)
+        st = streams[i & 1]
+        with torch.cuda.stream(st):
+            xi = xin[i & 1][:m]
+            ci = cout[i & 1][:m * per_img]
+            xi.copy_(host_images[s0:s0 + m], non_blocking=True)
+            dct16a_forward(xi, ci, desc_of(xi), st)
+            host_coef[s0 * per_img:(s0 + m) * per_img].copy_(ci, non_blocking=True)
+    for s in streams:
+        cur.wait_stream(s)
+    return bufs

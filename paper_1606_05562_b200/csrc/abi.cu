@@ -1,0 +1,207 @@
+// abi.cu — the C ABI of include/dct16a.h: argument validation (synchronous,
+// before any launch), error codes, thread-local error text, tensor-map
+// encoding through the driver entry point, and dispatch to the launchers.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <mutex>
+
+#include "internal.h"
+
+namespace dct16a {
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Validate a descriptor and fill the geometry.  Reading of the shape/pitch rules:
+// SURVEY.md §8(b) conventions, restated in include/dct16a.h.
+int check_desc(const dct16a_desc* d, Geom* g) {
+    if (!d) return fail(DCT16A_ENULL, "desc is NULL");
+    if (d->bit_depth != 8 && d->bit_depth != 10)
+        return fail(DCT16A_EDOMAIN, "bit_depth %d not in {8, 10}", d->bit_depth);
+    if (d->width <= 0 || d->height <= 0 || (d->width % 16) || (d->height % 16))
+        return fail(DCT16A_ESHAPE, "width %d / height %d must be positive multiples of 16", d->width,
+                    d->height);
+    if (d->batch < 1) return fail(DCT16A_ESHAPE, "batch %d < 1", d->batch);
+    if (d->valid_height <= 0 || d->valid_height > d->height)
+        return fail(DCT16A_ESHAPE, "valid_height %d outside (0, %d]", d->valid_height, d->height);
+    if (d->reserved != 0) return fail(DCT16A_EDOMAIN, "desc.reserved must be 0");
+    const int elem = d->bit_depth == 8 ? 1 : 2;
+    if (d->pitch_bytes < static_cast<int64_t>(d->width) * elem || (d->pitch_bytes % 16))
+        return fail(DCT16A_EPITCH, "pitch %lld must be >= width*elem and a multiple of 16",
+                    static_cast<long long>(d->pitch_bytes));
+    if (d->image_stride_bytes % 16)
+        return fail(DCT16A_EPITCH, "image_stride %lld not a multiple of 16",
+                    static_cast<long long>(d->image_stride_bytes));
+    if (d->batch > 1 && d->image_stride_bytes < d->pitch_bytes * d->height)
+        return fail(DCT16A_EPITCH, "image_stride %lld < pitch*height",
+                    static_cast<long long>(d->image_stride_bytes));
+    if (d->pitch_bytes >= (int64_t(1) << 40) || d->image_stride_bytes >= (int64_t(1) << 40))
+        return fail(DCT16A_EPITCH, "pitch/stride too large for a tensor map");
+    g->W = d->width;
+    g->H = d->height;
+    g->VH = d->valid_height;
+    g->N = d->batch;
+    g->bits = d->bit_depth;
+    g->BX = d->width / 16;
+    g->BY = d->height / 16;
+    g->elem = elem;
+    g->pitch = d->pitch_bytes;
+    g->istride = d->batch > 1 ? d->image_stride_bytes
+                              : (d->image_stride_bytes > 0 ? d->image_stride_bytes
+                                                           : d->pitch_bytes * d->height);
+    g->nblocks = static_cast<int64_t>(g->N) * g->BX * g->BY;
+    return 0;
+}
+
+int check_quant(const dct16a_quant* q) {
+    if (!q) return fail(DCT16A_ENULL, "quant is NULL");
+    if (q->reserved != 0) return fail(DCT16A_EDOMAIN, "quant.reserved must be 0");
+    if (q->mode == DCT16A_ZONAL) {
+        if (q->r < 1 || q->r > 256) return fail(DCT16A_EDOMAIN, "r=%d outside [1, 256]", q->r);
+    } else if (q->mode == DCT16A_UNIFORM) {
+        if (q->step < 1 || q->step > 65535)
+            return fail(DCT16A_EDOMAIN, "step=%d outside [1, 65535]", q->step);
+    } else {
+        return fail(DCT16A_EDOMAIN, "unknown quantiser mode %d", q->mode);
+    }
+    return 0;
+}
+
+int check_ptr(const void* p, const char* name) {
+    if (!p) return fail(DCT16A_ENULL, "%s is NULL", name);
+    if (!aligned16(p)) return fail(DCT16A_EALIGN, "%s is not 16-byte aligned", name);
+    return 0;
+}
+
+int launched(int rc, const char* what) {
+    if (rc == 0) {
+        g_err[0] = 0;
+        return DCT16A_OK;
+    }
+    if (rc < 0) return fail(rc, "%s: tensor-map encode failed", what);
+    return fail(DCT16A_ECUDA, "%s: %s", what, cudaGetErrorString(static_cast<cudaError_t>(rc)));
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+}  // namespace
+
+int encode_tiled(CUtensorMap* map, CUtensorMapDataType dt, uint32_t rank, const void* gaddr,
+                 const uint64_t* dims, const uint64_t* strides_bytes, const uint32_t* box,
+                 CUtensorMapSwizzle swz, CUtensorMapL2promotion promo) {
+    EncodeFn fn = get_encode();
+    if (!fn) return -1;
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = fn(map, dt, rank, const_cast<void*>(gaddr), reinterpret_cast<const cuuint64_t*>(dims),
+                    reinterpret_cast<const cuuint64_t*>(strides_bytes), reinterpret_cast<const cuuint32_t*>(box),
+                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return static_cast<int>(r);
+}
+
+int num_sms() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static int cache[64] = {0};
+    if (dev >= 0 && dev < 64 && cache[dev]) return cache[dev];
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (dev >= 0 && dev < 64) cache[dev] = n;
+    return n;
+}
+
+}  // namespace dct16a
+
+using namespace dct16a;
+
+extern "C" {
+
+DCT16A_API int dct16a_forward(const void* src, const dct16a_desc* desc, int32_t* coef, void* stream) {
+    Geom g;
+    int rc;
+    if ((rc = check_desc(desc, &g))) return rc;
+    if ((rc = check_ptr(src, "src")) || (rc = check_ptr(coef, "coef"))) return rc;
+    return launched(launch_forward(src, g, coef, static_cast<cudaStream_t>(stream)), "dct16a_forward");
+}
+
+DCT16A_API int dct16a_quantize(const int32_t* coef, const dct16a_desc* desc, const dct16a_quant* quant,
+                               int32_t* qcoef, float* scaled, void* stream) {
+    Geom g;
+    int rc;
+    if ((rc = check_desc(desc, &g)) || (rc = check_quant(quant))) return rc;
+    if ((rc = check_ptr(coef, "coef")) || (rc = check_ptr(qcoef, "qcoef"))) return rc;
+    if (scaled && !aligned16(scaled)) return fail(DCT16A_EALIGN, "scaled is not 16-byte aligned");
+    return launched(launch_quantize(coef, g, *quant, qcoef, scaled, static_cast<cudaStream_t>(stream)),
+                    "dct16a_quantize");
+}
+
+DCT16A_API int dct16a_inverse(const int32_t* qcoef, const dct16a_desc* desc, const dct16a_quant* quant,
+                              void* recon, void* stream) {
+    Geom g;
+    int rc;
+    if ((rc = check_desc(desc, &g)) || (rc = check_quant(quant))) return rc;
+    if ((rc = check_ptr(qcoef, "qcoef")) || (rc = check_ptr(recon, "recon"))) return rc;
+    return launched(launch_inverse(qcoef, g, *quant, recon, static_cast<cudaStream_t>(stream)),
+                    "dct16a_inverse");
+}
+
+DCT16A_API int dct16a_psnr(const void* ref, const void* test, const dct16a_desc* desc, uint64_t* sse,
+                           double* psnr, void* stream) {
+    Geom g;
+    int rc;
+    if ((rc = check_desc(desc, &g))) return rc;
+    if ((rc = check_ptr(ref, "ref")) || (rc = check_ptr(test, "test"))) return rc;
+    if (!sse) return fail(DCT16A_ENULL, "sse is NULL");
+    if (reinterpret_cast<uintptr_t>(sse) & 7u) return fail(DCT16A_EALIGN, "sse is not 8-byte aligned");
+    if (psnr && (reinterpret_cast<uintptr_t>(psnr) & 7u)) return fail(DCT16A_EALIGN, "psnr not 8-byte aligned");
+    return launched(launch_psnr(ref, test, g, sse, psnr, static_cast<cudaStream_t>(stream)), "dct16a_psnr");
+}
+
+DCT16A_API int dct16a_codec(const void* src, const dct16a_desc* desc, const dct16a_quant* quant, void* recon,
+                            uint64_t* sse, double* psnr, void* stream) {
+    Geom g;
+    int rc;
+    if ((rc = check_desc(desc, &g)) || (rc = check_quant(quant))) return rc;
+    if ((rc = check_ptr(src, "src"))) return rc;
+    if (recon && !aligned16(recon)) return fail(DCT16A_EALIGN, "recon is not 16-byte aligned");
+    if (recon == src) return fail(DCT16A_EDOMAIN, "recon must not alias src");
+    if (!sse) return fail(DCT16A_ENULL, "sse is NULL");
+    if (reinterpret_cast<uintptr_t>(sse) & 7u) return fail(DCT16A_EALIGN, "sse is not 8-byte aligned");
+    if (psnr && (reinterpret_cast<uintptr_t>(psnr) & 7u)) return fail(DCT16A_EALIGN, "psnr not 8-byte aligned");
+    return launched(launch_codec(src, g, *quant, recon, sse, psnr, static_cast<cudaStream_t>(stream)),
+                    "dct16a_codec");
+}
+
+DCT16A_API const char* dct16a_last_error(void) { return g_err; }
+
+DCT16A_API const char* dct16a_version(void) { return "dct16a 0.1.0 sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,279 @@
+// forward.cu — K1: the standalone forward 2-D transform Z = T·X·Tᵀ over every
+// 16x16 block (row pass, transposition, column pass as in
+// the paper's 2-D architecture), int32 block-major out.
+//
+// B200 design:
+//  * one thread owns one 16x16 block; a warp owns a tile of 32 horizontally
+//    adjacent blocks of one 16-row strip; warps are persistent and walk tiles
+//    with a stride of the total warp count;
+//  * TMA (cp.async.bulk.tensor) streams the 16-row strip tile into a 2-stage
+//    per-warp smem ring (mbarrier complete_tx); pixels are read back with
+//    128-bit ld.shared (conflict-free: a phase of 8 lanes reads 128 contiguous
+//    bytes);
+//  * both 1-D passes run the 60-add network of Eq. (1) on 16-bit SWAR pairs
+//    (two vectors per 32-bit register, lo + hi·2^16), so the 2-D transform
+//    costs 8+8 networks = 960 adds per block instead of 1920.  The column pass
+//    runs first (pairs of adjacent columns, |T·X| <= 16·maxpix fits a lane);
+//    the transposition buffer of the paper is a register byte-permute (PRMT)
+//    that turns "column pair of one row" into "row pair of one column";
+//    the row pass then yields two rows of Z per network (8-bit: Z_00 in
+//    [0, 65280] is the only entry outside int16 and is decoded unsigned);
+//  * each Z row pair (128 B per block) is staged in smem in the TMA 128-byte
+//    swizzle (conflict-free STS) and written by one TMA tensor store of
+//    32 blocks x 128 B; two staging buffers alternate (bulk async-groups).
+#include <cuda.h>
+#include <stdint.h>
+
+#include "internal.h"
+#include "net16.cuh"
+#include "ptx.cuh"
+
+namespace dct16a {
+namespace {
+
+constexpr int kTile = 32;    // blocks per warp tile = lanes
+constexpr int kStages = 2;   // input ring depth per warp
+constexpr int kOutBuf = 2;   // staging buffers per warp (4 KB each)
+constexpr int kOutBytes = kTile * 128;
+
+template <int ELEM>
+struct FwdCfg {
+    static constexpr int kWarps = ELEM == 1 ? 4 : 5;
+    static constexpr int kMinCtas = ELEM == 1 ? 2 : 1;
+    static constexpr int kStageBytes = 16 * 512 * ELEM;   // 16 rows x 512 px
+    static constexpr int kWarpBytes = kStages * kStageBytes + kOutBuf * kOutBytes;
+    static constexpr int kSmem = 1024 + kWarps * kWarpBytes + kWarps * kStages * 8;
+};
+
+struct FwdParams {
+    int W, BX, BY, tiles_per_strip, box_w;
+    long long n_tiles;
+};
+
+// Pad the dynamic smem base to 1024 B (128-byte swizzle atoms) while keeping
+// the pointer derived from the __shared__ array, so the compiler emits LDS/STS.
+__device__ __forceinline__ uint8_t* align1024(uint8_t* smem_raw) {
+    return smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+}
+
+// Issue the TMA loads of tile `tix` into `stage` (one elected lane).
+template <int ELEM>
+__device__ __forceinline__ void issue_tile(const CUtensorMap* tin, const FwdParams& p, long long tix,
+                                           uint8_t* stage, uint64_t* bar, uint64_t pol) {
+    const long long strip = tix / p.tiles_per_strip;
+    const int tb = static_cast<int>(tix - strip * p.tiles_per_strip);
+    const int n = static_cast<int>(strip / p.BY);
+    const int by = static_cast<int>(strip - static_cast<long long>(n) * p.BY);
+    const int x0 = tb * kTile * 16;
+    const int nbox_max = 512 / p.box_w;
+    int nbox = 0;
+    for (int h = 0; h < nbox_max; ++h)
+        if (x0 + h * p.box_w < p.W) ++nbox;
+    mbar_arrive_expect_tx(bar, static_cast<uint32_t>(nbox * 16 * p.box_w * ELEM));
+    for (int h = 0; h < nbox; ++h)
+        tma_load_3d(stage + h * 16 * p.box_w * ELEM, tin, bar, x0 + h * p.box_w, by * 16, n, pol);
+}
+
+}  // namespace
+
+template <int ELEM>
+__global__ void __launch_bounds__(FwdCfg<ELEM>::kWarps * 32, FwdCfg<ELEM>::kMinCtas)
+    fwd_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+               const FwdParams p) {
+    using Cfg = FwdCfg<ELEM>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    uint8_t* wbase = smem + warp * Cfg::kWarpBytes;
+    uint8_t* outb = wbase + kStages * Cfg::kStageBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kWarps * Cfg::kWarpBytes) + warp * kStages;
+
+    const long long gw = static_cast<long long>(blockIdx.x) * Cfg::kWarps + warp;
+    const long long nw = static_cast<long long>(gridDim.x) * Cfg::kWarps;
+    const uint64_t pol = policy_evict_first();
+
+    if (lane == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+        prefetch_tmap(&tin);
+        prefetch_tmap(&tout);
+        for (int s = 0; s < kStages; ++s) {
+            const long long t = gw + s * nw;
+            if (t < p.n_tiles) issue_tile<ELEM>(&tin, p, t, wbase + s * Cfg::kStageBytes, &bars[s], pol);
+        }
+    }
+    __syncwarp();
+
+    // this lane's block inside the tile: box h, column offset inside the box
+    const int px = lane * 16;
+    const int lane_off = (px / p.box_w) * 16 * p.box_w * ELEM + (px % p.box_w) * ELEM;
+    const int row_pitch = p.box_w * ELEM;
+    int obuf = 0;
+    int it = 0;
+    for (long long tix = gw; tix < p.n_tiles; tix += nw, ++it) {
+        const int s = it % kStages;
+        uint8_t* stage = wbase + s * Cfg::kStageBytes;
+        mbar_wait(&bars[s], (it / kStages) & 1);
+
+        const long long strip = tix / p.tiles_per_strip;
+        const int bx0 = static_cast<int>(tix - strip * p.tiles_per_strip) * kTile;
+
+        // ---- column pass (SWAR: column pairs (2m, 2m+1) of one row per register)
+        uint32_t o[8][16];
+        if constexpr (ELEM == 1) {
+            uint32_t R[16][4];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const uint4 v = *reinterpret_cast<const uint4*>(stage + lane_off + i * row_pitch);
+                R[i][0] = v.x; R[i][1] = v.y; R[i][2] = v.z; R[i][3] = v.w;
+            }
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                uint32_t x[16], y[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    x[i] = __byte_perm(R[i][m >> 1], 0u, (m & 1) ? 0x4342 : 0x4140);
+                net_fwd(x, y);
+                // bias both lanes by 2^15 so every lane is a non-negative 16-bit
+                // field (|T·X| <= 4080): the byte permute below is then exact.
+#pragma unroll
+                for (int k = 0; k < 16; ++k) o[m][k] = y[k] + 0x80008000u;
+            }
+        } else {
+            uint32_t R[16][8];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const uint4 a = *reinterpret_cast<const uint4*>(stage + lane_off + i * row_pitch);
+                const uint4 b = *reinterpret_cast<const uint4*>(stage + lane_off + i * row_pitch + 16);
+                R[i][0] = a.x; R[i][1] = a.y; R[i][2] = a.z; R[i][3] = a.w;
+                R[i][4] = b.x; R[i][5] = b.y; R[i][6] = b.z; R[i][7] = b.w;
+            }
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                uint32_t x[16], y[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) x[i] = R[i][m];   // int16 pair = SWAR pair
+                net_fwd(x, y);
+#pragma unroll
+                for (int k = 0; k < 16; ++k) o[m][k] = y[k] + 0x80008000u;   // |T·X| <= 16368
+            }
+        }
+        __syncwarp();
+        // stage s fully consumed by every lane: refill it with the tile kStages ahead
+        if (lane == 0) {
+            const long long nt = tix + kStages * nw;
+            if (nt < p.n_tiles) issue_tile<ELEM>(&tin, p, nt, stage, &bars[s], pol);
+        }
+
+        // ---- row pass, two rows of Z per step, staged + TMA-stored
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            int32_t z0[16], z1[16];   // rows 2r and 2r+1 of Z
+            if constexpr (ELEM == 1) {
+                uint32_t x[16], y[16];
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    x[2 * m] = __byte_perm(o[m][2 * r], o[m][2 * r + 1], 0x5410);
+                    x[2 * m + 1] = __byte_perm(o[m][2 * r], o[m][2 * r + 1], 0x7632);
+                }
+                net_fwd(x, y);
+                y[0] -= 0x00080000u;   // remove 16 x (2^15 + 2^31) bias of output l = 0
+#pragma unroll
+                for (int l = 0; l < 16; ++l) {
+                    int32_t lo;
+                    if (r == 0 && l == 0) lo = static_cast<int32_t>(y[l] & 0xFFFFu);   // Z_00 in [0, 65280]
+                    else lo = static_cast<int32_t>(static_cast<int16_t>(y[l] & 0xFFFFu));
+                    z0[l] = lo;
+                    z1[l] = static_cast<int32_t>(y[l] - static_cast<uint32_t>(lo)) >> 16;
+                }
+            } else {
+                int32_t x0[16], x1[16];
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    x0[2 * m] = static_cast<int32_t>(o[m][2 * r] & 0xFFFFu);
+                    x0[2 * m + 1] = static_cast<int32_t>(o[m][2 * r] >> 16);
+                    x1[2 * m] = static_cast<int32_t>(o[m][2 * r + 1] & 0xFFFFu);
+                    x1[2 * m + 1] = static_cast<int32_t>(o[m][2 * r + 1] >> 16);
+                }
+                net_fwd(x0, z0);
+                net_fwd(x1, z1);
+                z0[0] -= 16 * 32768;   // inputs carried a +2^15 bias
+                z1[0] -= 16 * 32768;
+            }
+            // staging buffer used two stores ago must have been read by the TMA
+            if (lane == 0) bulk_wait_read<kOutBuf - 1>();
+            __syncwarp();
+            uint8_t* ob = outb + obuf * kOutBytes + lane * 128;
+            const int sw = lane & 7;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                *reinterpret_cast<int4*>(ob + ((c ^ sw) << 4)) =
+                    make_int4(z0[4 * c], z0[4 * c + 1], z0[4 * c + 2], z0[4 * c + 3]);
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                *reinterpret_cast<int4*>(ob + (((c + 4) ^ sw) << 4)) =
+                    make_int4(z1[4 * c], z1[4 * c + 1], z1[4 * c + 2], z1[4 * c + 3]);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_4d(&tout, outb + obuf * kOutBytes, 0, bx0, r, static_cast<int32_t>(strip));
+                bulk_commit();
+            }
+            obuf ^= 1;
+        }
+    }
+    if (lane == 0) bulk_wait<0>();
+}
+
+namespace {
+
+template <int ELEM>
+int launch_fwd_t(const void* src, const Geom& g, int32_t* coef, cudaStream_t st) {
+    using Cfg = FwdCfg<ELEM>;
+    CUtensorMap tin, tout;
+    const int box_w = g.W < 256 ? g.W : 256;
+    {
+        const uint64_t dims[3] = {uint64_t(g.W), uint64_t(g.H), uint64_t(g.N)};
+        const uint64_t strides[2] = {uint64_t(g.pitch), uint64_t(g.istride)};
+        const uint32_t box[3] = {uint32_t(box_w), 16u, 1u};
+        int rc = encode_tiled(&tin, ELEM == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16,
+                              3, src, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+        if (rc) return DCT16A_ECUDA;
+    }
+    {
+        const uint64_t dims[4] = {32u, uint64_t(g.BX), 8u, uint64_t(g.N) * uint64_t(g.BY)};
+        const uint64_t strides[3] = {1024u, 128u, uint64_t(g.BX) * 1024u};
+        const uint32_t box[4] = {32u, uint32_t(g.BX < 32 ? g.BX : 32), 1u, 1u};
+        int rc = encode_tiled(&tout, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, coef, dims, strides, box,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+        if (rc) return DCT16A_ECUDA;
+    }
+    FwdParams p;
+    p.W = g.W;
+    p.BX = g.BX;
+    p.BY = g.BY;
+    p.tiles_per_strip = (g.BX + kTile - 1) / kTile;
+    p.box_w = box_w;
+    p.n_tiles = static_cast<long long>(g.N) * g.BY * p.tiles_per_strip;
+
+    static bool attr_set = false;   // idempotent; benign race
+    if (!attr_set) {
+        cudaFuncSetAttribute(fwd_kernel<ELEM>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+        attr_set = true;
+    }
+    const long long want = (p.n_tiles + Cfg::kWarps - 1) / Cfg::kWarps;
+    long long grid = static_cast<long long>(num_sms()) * Cfg::kMinCtas;
+    if (want < grid) grid = want;
+    fwd_kernel<ELEM><<<static_cast<unsigned>(grid), Cfg::kWarps * 32, Cfg::kSmem, st>>>(tin, tout, p);
+    return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace
+
+int launch_forward(const void* src, const Geom& g, int32_t* coef, cudaStream_t st) {
+    return g.elem == 1 ? launch_fwd_t<1>(src, g, coef, st) : launch_fwd_t<2>(src, g, coef, st);
+}
+
+}  // namespace dct16a

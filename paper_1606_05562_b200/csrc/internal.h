@@ -1,0 +1,41 @@
+// internal.h — private launcher interface between the C-ABI layer (abi.cu)
+// and the kernel translation units.  Not installed; not part of the ABI.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/dct16a.h"
+
+namespace dct16a {
+
+// Geometry of a validated image batch, in blocks.
+struct Geom {
+    int W, H, VH, N, bits;   // width, height, valid height, batch, bit depth
+    int BX, BY;              // blocks per row / column
+    int elem;                // bytes per pixel (1 or 2)
+    int64_t pitch, istride;  // bytes
+    int64_t nblocks;         // N·BY·BX
+};
+
+// Encodes a tiled tensor map through the driver entry point (no -lcuda link).
+// Returns 0 on success, a CUresult otherwise.
+int encode_tiled(CUtensorMap* map, CUtensorMapDataType dt, uint32_t rank, const void* gaddr,
+                 const uint64_t* dims, const uint64_t* strides_bytes, const uint32_t* box,
+                 CUtensorMapSwizzle swz, CUtensorMapL2promotion promo);
+
+int num_sms();
+
+// Launchers: return cudaError_t of the launch (cudaSuccess = 0) or a negative
+// DCT16A_E* code for encode failures.
+int launch_forward(const void* src, const Geom& g, int32_t* coef, cudaStream_t st);
+int launch_quantize(const int32_t* coef, const Geom& g, const dct16a_quant& q, int32_t* qcoef,
+                    float* scaled, cudaStream_t st);
+int launch_inverse(const int32_t* qcoef, const Geom& g, const dct16a_quant& q, void* recon,
+                   cudaStream_t st);
+int launch_psnr(const void* ref, const void* test, const Geom& g, uint64_t* sse, double* psnr,
+                cudaStream_t st);
+int launch_codec(const void* src, const Geom& g, const dct16a_quant& q, void* recon,
+                 uint64_t* sse, double* psnr, cudaStream_t st);
+
+}  // namespace dct16a

@@ -1,0 +1,105 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol that
+include/dct16a.h declares, and validates arguments synchronously (before any
+CUDA call) with the documented error codes."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_1606_05562_b200 as pkg
+from paper_1606_05562_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "dct16a.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"DCT16A_API\s+[\w\s\*]*?\b(dct16a_\w+)\s*\(", text)))
+
+
+def test_library_loads_and_exports_header_symbols():
+    L = pkg.lib()
+    syms = declared_symbols()
+    assert len(syms) == 7
+    for s in syms:
+        assert hasattr(L, s), s
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (dct16a_\w+)", out))
+    assert set(syms) <= exported
+    # nothing but the ABI is exported from the dct16a namespace
+    assert all(s.startswith("dct16a_") for s in exported)
+
+
+def test_version():
+    assert pkg.dct16a_version().startswith("dct16a ")
+    assert "sm_100a" in pkg.dct16a_version()
+
+
+def test_struct_layout_matches_header():
+    assert ctypes.sizeof(_lib.Desc) == 40
+    assert ctypes.sizeof(_lib.Quant) == 16
+
+
+def _call_forward(desc, src=16, coef=16):
+    L = pkg.lib()
+    return L.dct16a_forward(ctypes.c_void_p(src), ctypes.byref(desc), ctypes.c_void_p(coef), None)
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(width=0), -2), (dict(width=24), -2), (dict(height=-16), -2), (dict(batch=0), -2),
+    (dict(valid_height=0), -2), (dict(valid_height=32), -2), (dict(bit_depth=12), -5),
+    (dict(pitch_bytes=8), -3), (dict(pitch_bytes=72), -3), (dict(image_stride_bytes=8), -3),
+])
+def test_forward_validation_codes(kw, code):
+    base = dict(width=64, height=16, valid_height=16, batch=2, bit_depth=8, pitch_bytes=64,
+                image_stride_bytes=1024)
+    base.update(kw)
+    d = _lib.Desc(base["width"], base["height"], base["valid_height"], base["batch"], base["bit_depth"], 0,
+                  base["pitch_bytes"], base["image_stride_bytes"])
+    assert _call_forward(d) == code
+    assert pkg.dct16a_last_error() != ""
+
+
+def test_pointer_validation():
+    d = _lib.make_desc(64, 16, 1, 8)
+    assert _call_forward(d, src=0) == -1            # ENULL
+    assert _call_forward(d, src=8) == -4            # EALIGN
+    assert _call_forward(d, coef=4) == -4
+    L = pkg.lib()
+    assert L.dct16a_forward(ctypes.c_void_p(16), None, ctypes.c_void_p(16), None) == -1
+
+
+@pytest.mark.parametrize("q,code", [
+    (dict(mode=0, r=0), -5), (dict(mode=0, r=257), -5), (dict(mode=1, step=0), -5),
+    (dict(mode=7), -5), (dict(mode=1, step=70000), -5)])
+def test_quant_validation(q, code):
+    d = _lib.make_desc(64, 16, 1, 8)
+    qq = _lib.Quant(q.get("mode", 0), q.get("r", 16), q.get("step", 16), 0)
+    L = pkg.lib()
+    rc = L.dct16a_codec(ctypes.c_void_p(16), ctypes.byref(d), ctypes.byref(qq), None, ctypes.c_void_p(16),
+                        None, None)
+    assert rc == code
+    rc = L.dct16a_quantize(ctypes.c_void_p(16), ctypes.byref(d), ctypes.byref(qq), ctypes.c_void_p(16),
+                           None, None)
+    assert rc == code
+
+
+def test_codec_pointer_rules():
+    d = _lib.make_desc(64, 16, 1, 8)
+    q = _lib.make_quant("zonal", 16)
+    L = pkg.lib()
+    assert L.dct16a_codec(ctypes.c_void_p(16), ctypes.byref(d), ctypes.byref(q), None, None, None, None) == -1
+    assert L.dct16a_codec(ctypes.c_void_p(16), ctypes.byref(d), ctypes.byref(q), None, ctypes.c_void_p(12),
+                          None, None) == -4
+    assert L.dct16a_codec(ctypes.c_void_p(32), ctypes.byref(d), ctypes.byref(q), ctypes.c_void_p(32),
+                          ctypes.c_void_p(16), None, None) == -5   # recon aliases src
+
+
+def test_binding_rejects_cpu_tensors():
+    torch = pytest.importorskip("torch")
+    x = torch.zeros((1, 16, 16), dtype=torch.uint8)
+    with pytest.raises(ValueError):
+        pkg.dct16a_forward(x, torch.zeros((1, 16, 16), dtype=torch.int32))

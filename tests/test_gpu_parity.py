@@ -1,0 +1,252 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Bar: integer Z, quantised integer stages,
+reconstructed pixels and SSE bit-exact; float32 scaled stages within 1e-5
+relative (and exactly 0 where the oracle is 0); PSNR within 1e-3 dB.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import codec as oc
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU box
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1606_05562_b200 as pkg  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def oracle_Z(imgs):
+    return oc.forward(oc.to_blocks(imgs.astype(np.int64))).reshape(-1, 16, 16)
+
+
+def gpu_Z(imgs_t, desc=None):
+    n, h, w = imgs_t.shape
+    out = torch.empty((n * (h // 16) * (w // 16), 16, 16), dtype=torch.int32, device=DEV)
+    pkg.dct16a_forward(imgs_t, out, desc if desc is not None else pkg.desc_of(imgs_t))
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def u8_cases():
+    yield "cfg1", synth.image_u8(0)[None]
+    yield "adversarial", synth.adversarial_u8(64, 64)
+    yield "ragged17x3", synth.batch_u8([5, 6, 7], 48, 272)         # BX=17: tile of 32 is ragged
+    yield "wide", synth.batch_u8([8], 32, 1920)                    # 120 blocks: 3 full tiles + 24
+    yield "tiny", synth.batch_u8([9], 16, 16)
+    yield "narrow", synth.batch_u8([10, 11], 64, 48)
+    rng = np.random.default_rng(3)
+    yield "uniform-noise", rng.integers(0, 256, size=(4, 64, 96)).astype(np.uint8)
+
+
+@pytest.mark.parametrize("name,imgs", list(u8_cases()), ids=lambda v: v if isinstance(v, str) else "")
+def test_forward_u8_bit_exact(name, imgs):
+    assert np.array_equal(gpu_Z(to_dev(imgs)), oracle_Z(imgs))
+
+
+def test_forward_10bit_bit_exact():
+    imgs = synth.frames_10bit([0, 1], H=64, W=272, workers=1)
+    adv = synth.adversarial_u8(48, 80, bit_depth=10)
+    for x in (imgs, adv):
+        assert np.array_equal(gpu_Z(to_dev(x)), oracle_Z(x))
+
+
+def test_forward_pitched_and_strided():
+    big = synth.batch_u8([12, 13, 14], 80, 400)
+    t = to_dev(big)[:, 8:72, 32:288]                   # pitch 400 > width 256, stride 32000
+    view = big[:, 8:72, 32:288]
+    assert np.array_equal(gpu_Z(t), oracle_Z(view))
+    f = synth.frames_10bit([3], H=48, W=320, workers=1)
+    t10 = to_dev(f)[:, :, 16:240]
+    assert np.array_equal(gpu_Z(t10), oracle_Z(f[:, :, 16:240]))
+
+
+def _quant_run(imgs, q, bit_depth):
+    x = to_dev(imgs)
+    d = pkg.desc_of(x, bit_depth)
+    n, h, w = imgs.shape
+    nb = n * (h // 16) * (w // 16)
+    coef = torch.empty((nb, 16, 16), dtype=torch.int32, device=DEV)
+    qc = torch.empty_like(coef)
+    sc = torch.empty((nb, 16, 16), dtype=torch.float32, device=DEV)
+    rec = torch.empty_like(x)
+    pkg.dct16a_forward(x, coef, d)
+    pkg.dct16a_quantize(coef, qc, q, d, sc)
+    pkg.dct16a_inverse(qc, rec, q, d)
+    torch.cuda.synchronize()
+    return coef.cpu().numpy(), qc.cpu().numpy(), sc.cpu().numpy(), rec.cpu().numpy()
+
+
+def _check_scaled(got, want):
+    want = want.reshape(got.shape)
+    zero = want == 0
+    assert np.all(got[zero] == 0)
+    rel = np.abs(got[~zero] - want[~zero]) / np.abs(want[~zero])
+    assert rel.max() <= 1e-5, rel.max()
+
+
+@pytest.mark.parametrize("r", [1, 2, 15, 16, 17, 32, 64, 128, 255, 256])
+def test_zonal_stages_and_inverse(r):
+    imgs = np.concatenate([synth.batch_u8([20, 21], 64, 64), synth.adversarial_u8(64, 64)])
+    q = pkg.make_quant("zonal", r)
+    Z, qc, sc, rec = _quant_run(imgs, q, 8)
+    X = oc.to_blocks(imgs.astype(np.int64))
+    ref = oc.zonal_codec(X, r)
+    assert np.array_equal(Z, ref["Z"].reshape(Z.shape))
+    assert np.array_equal(qc, ref["Zm"].reshape(qc.shape))
+    _check_scaled(sc, ref["scaled"])
+    assert np.array_equal(rec, oc.from_blocks(ref["recon"]))
+    if r == 256:
+        assert np.array_equal(rec, imgs)
+
+
+@pytest.mark.parametrize("step", [1, 5, 16, 64])
+def test_uniform_stages_and_inverse(step):
+    imgs = np.concatenate([synth.frames_10bit([4, 5], H=64, W=96, workers=1),
+                           synth.adversarial_u8(64, 96, bit_depth=10)])
+    q = pkg.make_quant("uniform", step=step)
+    Z, qc, sc, rec = _quant_run(imgs, q, 10)
+    X = oc.to_blocks(imgs.astype(np.int64))
+    ref = oc.uniform_codec(X, step, 10)
+    assert np.array_equal(Z, ref["Z"].reshape(Z.shape))
+    assert np.array_equal(qc, ref["q"].reshape(qc.shape))
+    _check_scaled(sc, ref["scaled"])
+    assert np.array_equal(rec, oc.from_blocks(ref["recon"]))
+
+
+def test_uniform_forced_ties():
+    # coefficients exactly on a rounding tie in the rational cells must round away
+    T = np.array(oc.T)
+    g = np.diag(T @ T.T)
+    Zs = np.zeros((1, 16, 16), dtype=np.int32)
+    want = np.zeros((1, 16, 16), dtype=np.int64)
+    step = 16
+    rng = np.random.default_rng(0)
+    for k in range(16):
+        for l in range(16):
+            G = int(g[k] * g[l])
+            r = math.isqrt(G)
+            m = int(rng.integers(0, 400))
+            s = 1 if rng.random() < 0.5 else -1
+            if r * r == G:
+                z = (2 * m + 1) * step * r // 2
+            else:
+                z = int(rng.integers(0, 200000))
+            Zs[0, k, l] = s * z
+    want = oc.uniform_q(Zs.astype(np.int64), step)
+    coef = to_dev(Zs)
+    qc = torch.empty_like(coef)
+    d = pkg.make_desc(16, 16, 1, 10)
+    pkg.dct16a_quantize(coef, qc, pkg.make_quant("uniform", step=step), d)
+    torch.cuda.synchronize()
+    assert np.array_equal(qc.cpu().numpy(), want)
+
+
+def test_psnr_kernel():
+    a = synth.batch_u8([30, 31, 32], 64, 80)
+    b = a.copy()
+    b[0] ^= 1
+    b[1, 40:, :] = 0
+    x, y = to_dev(a), to_dev(b)
+    sse = torch.empty(3, dtype=torch.int64, device=DEV)
+    ps = torch.empty(3, dtype=torch.float64, device=DEV)
+    pkg.dct16a_psnr(x, y, sse, ps)
+    torch.cuda.synchronize()
+    want = oc.sse(a, b)
+    assert sse.cpu().tolist() == want
+    for got, s in zip(ps.cpu().tolist(), want):
+        exp = oc.psnr_from_sse(s, 64 * 80, 8)
+        assert (math.isinf(got) and math.isinf(exp)) or abs(got - exp) < 1e-3
+    # valid_height excludes rows
+    d = pkg.desc_of(x, valid_height=32)
+    pkg.dct16a_psnr(x, y, sse, ps, desc=d)
+    torch.cuda.synchronize()
+    assert sse.cpu().tolist() == oc.sse(a, b, 32)
+
+
+def _codec_check(imgs, mode, bit_depth, r=16, step=16, valid_height=None):
+    x = to_dev(imgs)
+    rec, sse, ps = pkg.codec(x, mode, r=r, step=step, valid_height=valid_height)
+    torch.cuda.synchronize()
+    ref = oc.codec_images(imgs, mode, r=r, step=step, bit_depth=bit_depth, valid_height=valid_height)
+    assert np.array_equal(rec.cpu().numpy(), ref["recon_img"])
+    assert sse.cpu().tolist() == ref["sse"]
+    for got, exp in zip(ps.cpu().tolist(), ref["psnr"]):
+        assert (math.isinf(got) and math.isinf(exp)) or abs(got - exp) < 1e-3
+    return rec
+
+
+def test_codec_config1():
+    _codec_check(synth.image_u8(0)[None], "zonal", 8, r=16)
+
+
+@pytest.mark.parametrize("r", [1, 32, 100, 256])
+def test_codec_zonal_varied(r):
+    imgs = np.concatenate([synth.batch_u8([40, 41], 48, 272), synth.adversarial_u8(48, 272)])
+    _codec_check(imgs, "zonal", 8, r=r)
+
+
+def test_codec_zonal_padded_valid_height():
+    v = synth.video_u8(3, H=56, W=96, pad_to=64, workers=1)
+    _codec_check(v, "zonal", 8, r=32, valid_height=56)
+
+
+def test_codec_uniform():
+    f = np.concatenate([synth.frames_10bit([6, 7], H=64, W=128, workers=1),
+                        synth.adversarial_u8(64, 128, bit_depth=10)])
+    _codec_check(f, "uniform", 10, step=16)
+
+
+def test_codec_equals_chain():
+    imgs = synth.batch_u8([50, 51], 64, 64)
+    for mode, r, step, bd, src in [("zonal", 16, 16, 8, imgs),
+                                   ("uniform", 16, 16, 10, synth.frames_10bit([8], H=64, W=64, workers=1))]:
+        q = pkg.make_quant(mode, r, step)
+        _, _, _, rec_chain = _quant_run(src, q, bd)
+        rec = _codec_check(src, mode, bd, r=r, step=step)
+        assert np.array_equal(rec.cpu().numpy(), rec_chain)
+
+
+def test_codec_without_recon_output():
+    img = synth.image_u8(1)[None]
+    x = to_dev(img)
+    _, sse, ps = pkg.codec(x, "zonal", r=16, want_recon=False)
+    torch.cuda.synchronize()
+    assert sse.cpu().tolist() == oc.codec_images(img, "zonal", r=16)["sse"]
+
+
+# ------------------------------------------------- full-size configurations
+@pytest.mark.slow
+def test_config2_full_size_sampled():
+    """Config 2 at full size (4096 x 512² u8) in the launch configuration that
+    bench.py times: sampled blocks checked against the oracle one by one, and
+    properties that hold for every block checked on all 4.19M blocks."""
+    n = 4096
+    imgs = synth.batch_u8(range(n), 512, 512)
+    x = to_dev(imgs)
+    coef = pkg.forward(x)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(2)
+    idx = rng.choice(coef.shape[0], size=3000, replace=False)
+    got = coef[torch.from_numpy(idx).to(DEV)].cpu().numpy()
+    Xb = oc.to_blocks(imgs.astype(np.int64)).reshape(-1, 16, 16)
+    assert np.array_equal(got, oc.forward(Xb[idx]))
+    # every block: DC = block sum, integer Parseval sum W·Z² = 2304·sum X²
+    T = np.array(oc.T)
+    g = np.diag(T @ T.T)
+    W = torch.from_numpy((2304 // np.outer(g, g)).astype(np.int64)).to(DEV)
+    for s in range(0, coef.shape[0], 1 << 20):
+        z = coef[s:s + (1 << 20)].to(torch.int64)
+        xb = x.view(n, 32, 16, 32, 16).permute(0, 1, 3, 2, 4).reshape(-1, 16, 16)[s:s + (1 << 20)].to(torch.int64)
+        assert torch.equal(z[:, 0, 0], xb.sum(dim=(1, 2)))
+        assert torch.equal((W * z * z).sum(dim=(1, 2)), 2304 * (xb * xb).sum(dim=(1, 2)))
