@@ -23,6 +23,7 @@
 //    32 blocks x 128 B; two staging buffers alternate (bulk async-groups).
 #include <cuda.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "internal.h"
 #include "net16.cuh"
@@ -33,15 +34,29 @@ namespace {
 
 constexpr int kTile = 32;    // blocks per warp tile = lanes
 constexpr int kStages = 2;   // input ring depth per warp
-constexpr int kOutBuf = 2;   // staging buffers per warp (4 KB each)
-constexpr int kOutBytes = kTile * 128;
 
-template <int ELEM>
+// Output paths (SM = store mode):
+//  0: TMA tensor store of one Z row pair (32 blocks x 128 B = 4 KB), 2 buffers
+//  1: as 0 with 4 buffers
+//  2: smem transpose + coalesced 128-bit st.global (LSU path), 1 buffer
+//  3: TMA tensor store of two row pairs (8 KB), 2 buffers
+//  4: TMA tensor store of four row pairs (16 KB), 2 buffers
+//  5: TMA tensor store of the whole tile (8 row pairs, 32 KB), 1 buffer
+template <int SM>
+struct StoreCfg {
+    static constexpr int kBufs = SM == 1 ? 4 : ((SM == 2 || SM == 5) ? 1 : 2);
+    static constexpr int kPairs = SM == 3 ? 2 : (SM == 4 ? 4 : (SM == 5 ? 8 : 1));   // row pairs per store
+    static constexpr int kBytes = kTile * 128 * kPairs;
+};
+
+template <int ELEM, int SM>
 struct FwdCfg {
-    static constexpr int kWarps = ELEM == 1 ? 4 : 5;
-    static constexpr int kMinCtas = ELEM == 1 ? 2 : 1;
     static constexpr int kStageBytes = 16 * 512 * ELEM;   // 16 rows x 512 px
-    static constexpr int kWarpBytes = kStages * kStageBytes + kOutBuf * kOutBytes;
+    static constexpr int kWarpBytes = kStages * kStageBytes + StoreCfg<SM>::kBufs * StoreCfg<SM>::kBytes;
+    // as many warps as the 227 KB of shared memory per SM allows, 4 or 5 per CTA
+    static constexpr int kWarpsPerSm = (227 * 1024 - 2048) / kWarpBytes;
+    static constexpr int kWarps = kWarpsPerSm >= 8 ? 4 : (kWarpsPerSm >= 5 ? 5 : kWarpsPerSm);
+    static constexpr int kMinCtas = kWarpsPerSm >= 8 ? 2 : 1;
     static constexpr int kSmem = 1024 + kWarps * kWarpBytes + kWarps * kStages * 8;
 };
 
@@ -76,11 +91,12 @@ __device__ __forceinline__ void issue_tile(const CUtensorMap* tin, const FwdPara
 
 }  // namespace
 
-template <int ELEM>
-__global__ void __launch_bounds__(FwdCfg<ELEM>::kWarps * 32, FwdCfg<ELEM>::kMinCtas)
+template <int ELEM, int SM>
+__global__ void __launch_bounds__(FwdCfg<ELEM, SM>::kWarps * 32, FwdCfg<ELEM, SM>::kMinCtas)
     fwd_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
-               const FwdParams p) {
-    using Cfg = FwdCfg<ELEM>;
+               int32_t* __restrict__ coef, const FwdParams p) {
+    using Cfg = FwdCfg<ELEM, SM>;
+    using SC = StoreCfg<SM>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     const int warp = threadIdx.x >> 5;
@@ -118,6 +134,8 @@ __global__ void __launch_bounds__(FwdCfg<ELEM>::kWarps * 32, FwdCfg<ELEM>::kMinC
 
         const long long strip = tix / p.tiles_per_strip;
         const int bx0 = static_cast<int>(tix - strip * p.tiles_per_strip) * kTile;
+        const int nvalid = p.BX - bx0 < kTile ? p.BX - bx0 : kTile;   // blocks of this tile inside the strip
+        int4* tile_dst = reinterpret_cast<int4*>(coef) + (strip * p.BX + bx0) * 64 + (lane & 7) + (lane >> 3) * 64;
 
         // ---- column pass (SWAR: column pairs (2m, 2m+1) of one row per register)
         uint32_t o[8][16];
@@ -201,10 +219,14 @@ __global__ void __launch_bounds__(FwdCfg<ELEM>::kWarps * 32, FwdCfg<ELEM>::kMinC
                 z0[0] -= 16 * 32768;   // inputs carried a +2^15 bias
                 z1[0] -= 16 * 32768;
             }
-            // staging buffer used two stores ago must have been read by the TMA
-            if (lane == 0) bulk_wait_read<kOutBuf - 1>();
+            const int half = r % SC::kPairs;   // position of this row pair inside its store
+            if (half == 0 && SM != 2) {
+                // the buffer about to be reused must have been read by its TMA store
+                if (lane == 0) bulk_wait_read<SC::kBufs - 1>();
+            }
             __syncwarp();
-            uint8_t* ob = outb + obuf * kOutBytes + lane * 128;
+            uint8_t* buf = outb + obuf * SC::kBytes + half * (kTile * 128);
+            uint8_t* ob = buf + lane * 128;
             const int sw = lane & 7;
 #pragma unroll
             for (int c = 0; c < 4; ++c)
@@ -214,13 +236,28 @@ __global__ void __launch_bounds__(FwdCfg<ELEM>::kWarps * 32, FwdCfg<ELEM>::kMinC
             for (int c = 0; c < 4; ++c)
                 *reinterpret_cast<int4*>(ob + (((c + 4) ^ sw) << 4)) =
                     make_int4(z1[4 * c], z1[4 * c + 1], z1[4 * c + 2], z1[4 * c + 3]);
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-                tma_store_4d(&tout, outb + obuf * kOutBytes, 0, bx0, r, static_cast<int32_t>(strip));
-                bulk_commit();
+            if constexpr (SM == 2) {
+                __syncwarp();
+                // lanes 8j..8j+7 move the 128 B row pair of block 4i+j: one warp
+                // instruction writes four full 128-byte lines
+                const uint8_t* src = buf + (lane >> 3) * 128;
+                const int s0 = ((lane & 7) ^ (lane >> 3)) << 4, s1 = ((lane & 7) ^ (4 + (lane >> 3))) << 4;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int4 v = *reinterpret_cast<const int4*>(src + i * 512 + ((i & 1) ? s1 : s0));
+                    if (4 * i + (lane >> 3) < nvalid) __stcs(tile_dst + i * 256 + r * 8, v);
+                }
+                __syncwarp();
+            } else if (half == SC::kPairs - 1) {
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_4d(&tout, buf - half * (kTile * 128), 0, bx0, r - half,
+                                 static_cast<int32_t>(strip));
+                    bulk_commit();
+                }
+                obuf = obuf + 1 == SC::kBufs ? 0 : obuf + 1;
             }
-            obuf ^= 1;
         }
     }
     if (lane == 0) bulk_wait<0>();
@@ -228,9 +265,9 @@ __global__ void __launch_bounds__(FwdCfg<ELEM>::kWarps * 32, FwdCfg<ELEM>::kMinC
 
 namespace {
 
-template <int ELEM>
+template <int ELEM, int SM>
 int launch_fwd_t(const void* src, const Geom& g, int32_t* coef, cudaStream_t st) {
-    using Cfg = FwdCfg<ELEM>;
+    using Cfg = FwdCfg<ELEM, SM>;
     CUtensorMap tin, tout;
     const int box_w = g.W < 256 ? g.W : 256;
     {
@@ -243,9 +280,10 @@ int launch_fwd_t(const void* src, const Geom& g, int32_t* coef, cudaStream_t st)
         if (rc) return DCT16A_ECUDA;
     }
     {
+        // coef viewed as {32 int32 of a row pair, block column bx, row pair, strip}
         const uint64_t dims[4] = {32u, uint64_t(g.BX), 8u, uint64_t(g.N) * uint64_t(g.BY)};
         const uint64_t strides[3] = {1024u, 128u, uint64_t(g.BX) * 1024u};
-        const uint32_t box[4] = {32u, uint32_t(g.BX < 32 ? g.BX : 32), 1u, 1u};
+        const uint32_t box[4] = {32u, uint32_t(g.BX < 32 ? g.BX : 32), uint32_t(StoreCfg<SM>::kPairs), 1u};
         int rc = encode_tiled(&tout, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, coef, dims, strides, box,
                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
         if (rc) return DCT16A_ECUDA;
@@ -260,20 +298,43 @@ int launch_fwd_t(const void* src, const Geom& g, int32_t* coef, cudaStream_t st)
 
     static bool attr_set = false;   // idempotent; benign race
     if (!attr_set) {
-        cudaFuncSetAttribute(fwd_kernel<ELEM>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+        cudaFuncSetAttribute(fwd_kernel<ELEM, SM>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
         attr_set = true;
     }
     const long long want = (p.n_tiles + Cfg::kWarps - 1) / Cfg::kWarps;
     long long grid = static_cast<long long>(num_sms()) * Cfg::kMinCtas;
     if (want < grid) grid = want;
-    fwd_kernel<ELEM><<<static_cast<unsigned>(grid), Cfg::kWarps * 32, Cfg::kSmem, st>>>(tin, tout, p);
+    fwd_kernel<ELEM, SM><<<static_cast<unsigned>(grid), Cfg::kWarps * 32, Cfg::kSmem, st>>>(tin, tout, coef, p);
     return static_cast<int>(cudaGetLastError());
+}
+
+// Output path of the forward kernel.  Default: 16 KB TMA tensor stores (mode 4),
+// measured fastest on config 2; DCT16A_FWD_STORE=0..5 selects
+// the other variants for experiments (profiles/r01_fwd_store_modes.md).
+int store_mode(int elem) {
+    static int m = [] {
+        const char* e = getenv("DCT16A_FWD_STORE");
+        return e ? atoi(e) : -1;
+    }();
+    return m >= 0 ? m : (elem == 1 ? 4 : 0);
+}
+
+template <int ELEM>
+int launch_fwd_e(const void* src, const Geom& g, int32_t* coef, cudaStream_t st) {
+    switch (store_mode(ELEM)) {
+        case 1: return launch_fwd_t<ELEM, 1>(src, g, coef, st);
+        case 2: return launch_fwd_t<ELEM, 2>(src, g, coef, st);
+        case 3: return launch_fwd_t<ELEM, 3>(src, g, coef, st);
+        case 4: return launch_fwd_t<ELEM, 4>(src, g, coef, st);
+        case 5: return launch_fwd_t<ELEM, 5>(src, g, coef, st);
+        default: return launch_fwd_t<ELEM, 0>(src, g, coef, st);
+    }
 }
 
 }  // namespace
 
 int launch_forward(const void* src, const Geom& g, int32_t* coef, cudaStream_t st) {
-    return g.elem == 1 ? launch_fwd_t<1>(src, g, coef, st) : launch_fwd_t<2>(src, g, coef, st);
+    return g.elem == 1 ? launch_fwd_e<1>(src, g, coef, st) : launch_fwd_e<2>(src, g, coef, st);
 }
 
 }  // namespace dct16a
