@@ -1,79 +1,49 @@
-// codec.cu — K4 quantize, K5 inverse, K6 SSE/PSNR and the fused codec
+// codec.cu — K4 quantize, K5 inverse, K6 SSE/PSNR and the generic fused codec
 // (forward -> quantise -> inverse -> reconstruct -> SSE) of the §4 pipeline,
 // PAPER.md:866-910, with S folded into the quantiser.
+// Exactness rules: quant.cuh.
 //
-// Exactness (readings A6, A9, A10):
-//  * zonal: N = Tᵀ·(W ⊙ Z ⊙ M_r)·T in int32 (|N| <= 7612·maxpix < 2^24),
-//    pixel = clamp(round_half_away(N / 2304)) decided on the integer N;
-//  * uniform: q = sign(Z)·m with m the largest integer such that
-//    (2m-1)²·Δ²·G <= 4·Z² (G = g_k·g_l), i.e. floor(|Z|/(Δ·sqrt G) + 1/2) with
-//    ties away from zero, decided in int64 after a float64 estimate;
-//    reconstruction Tᵀ·(Δ·q·s_k·s_l)·T in float64.
+// Fused codec layout (any r, zonal or uniform, 8- or 10-bit): one warp owns a
+// pair of horizontally adjacent blocks (lanes 0-15: block 2px, lanes 16-31:
+// block 2px+1), one lane per row/column; persistent CTAs walk a contiguous range
+// of block pairs so the per-image SSE is accumulated in registers and flushed
+// with one atomic per warp and image.  Both in-block transpositions (the
+// paper's transposition buffer) go through a per-warp smem
+// tile; per-lane constants (weights, mask, float64 scale factors) are computed
+// once per thread.
 #include <math.h>
-#include <type_traits>
 #include <stdint.h>
+
+#include <type_traits>
 
 #include "internal.h"
 #include "net16.cuh"
+#include "quant.cuh"
 #include "tables.cuh"
 
 namespace dct16a {
-namespace {
-
-__device__ __forceinline__ double inv_sqrt_G(int k, int l) {
-    return 1.0 / sqrt(static_cast<double>(g_of(k) * g_of(l)));
-}
-
-// exact uniform level (reading A9): floor(|Z|/(step·sqrt(G)) + 1/2), ties away
-__device__ __forceinline__ int32_t uniform_level(int32_t z, int k, int l, int step) {
-    const int64_t G = g_of(k) * g_of(l);
-    const int64_t az = z < 0 ? -static_cast<int64_t>(z) : static_cast<int64_t>(z);
-    const double est = static_cast<double>(az) * inv_sqrt_G(k, l) / static_cast<double>(step) + 0.5;
-    int64_t m = static_cast<int64_t>(floor(est));
-    const int64_t z4 = 4 * az * az;
-    const int64_t d2g = static_cast<int64_t>(step) * step * G;
-    if (m > 0 && (2 * m - 1) * (2 * m - 1) * d2g > z4) --m;
-    else if ((2 * m + 1) * (2 * m + 1) * d2g <= z4) ++m;
-    return static_cast<int32_t>(z < 0 ? -m : m);
-}
-
-__device__ __forceinline__ int zonal_pixel(int32_t N, int maxpix) {
-    // round half away of N/2304, clamped to [0, maxpix] (reading A6)
-    const int32_t v = N + 1152;
-    if (v <= 0) return 0;
-    const int32_t p = v / 2304;
-    return p > maxpix ? maxpix : p;
-}
-
-__device__ __forceinline__ int uniform_pixel(double a, int maxpix) {
-    if (!(a > 0.0)) return 0;            // round_half_away(a) <= 0 -> clamp 0
-    const double p = floor(a + 0.5);
-    return p > maxpix ? maxpix : static_cast<int>(p);
-}
 
 // ------------------------------------------------------------------ K4
-}  // namespace
-
 __global__ void quantize_kernel(const int4* __restrict__ coef, int4* __restrict__ qcoef,
-                                float4* __restrict__ scaled, long long n4, int mode, int r,
-                                int step) {
+                                float4* __restrict__ scaled, long long n4, int mode, int r, int step) {
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int4 z = coef[i];
         const int pos = static_cast<int>((i * 4) & 255);
         const int k = pos >> 4, l0 = pos & 15;
-        int zz[4] = {z.x, z.y, z.z, z.w};
+        const int zz[4] = {z.x, z.y, z.z, z.w};
         int qq[4];
         float ss[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const int l = l0 + e;
-            const double s = inv_sqrt_G(k, l);
+            const double s = s_of(k) * s_of(l);
             if (mode == DCT16A_ZONAL) {
                 qq[e] = zigzag_rank(k, l) < r ? zz[e] : 0;
                 ss[e] = static_cast<float>(s * static_cast<double>(qq[e]));
             } else {
-                qq[e] = uniform_level(zz[e], k, l, step);
+                const uint64_t d2g = static_cast<uint64_t>(step) * step * (g_of(k) * g_of(l));
+                qq[e] = uniform_level(zz[e], static_cast<float>(s / step), d2g);
                 ss[e] = static_cast<float>(s * static_cast<double>(zz[e]));
             }
         }
@@ -83,33 +53,16 @@ __global__ void quantize_kernel(const int4* __restrict__ coef, int4* __restrict_
 }
 
 namespace {
-// ------------------------------------------------ block addressing helpers
-struct BlkAddr {
-    long long img_off;  // byte offset of the block's top-left pixel
-    int n, row0;
-};
-
-__device__ __forceinline__ BlkAddr block_addr(long long b, const Geom& g) {
-    const long long per_img = static_cast<long long>(g.BY) * g.BX;
-    BlkAddr a;
-    a.n = static_cast<int>(b / per_img);
-    const long long rem = b - a.n * per_img;
-    const int by = static_cast<int>(rem / g.BX);
-    const int bx = static_cast<int>(rem - static_cast<long long>(by) * g.BX);
-    a.row0 = by * 16;
-    a.img_off = a.n * g.istride + static_cast<long long>(a.row0) * g.pitch + bx * 16LL * g.elem;
-    return a;
-}
 
 __device__ __forceinline__ void load_row(const uint8_t* p, int elem, int32_t (&x)[16]) {
     if (elem == 1) {
-        const uint4 v = *reinterpret_cast<const uint4*>(p);
+        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(p));
         const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int j = 0; j < 16; ++j) x[j] = (w[j >> 2] >> (8 * (j & 3))) & 0xFF;
     } else {
-        const uint4 a = *reinterpret_cast<const uint4*>(p);
-        const uint4 b = *reinterpret_cast<const uint4*>(p + 16);
+        const uint4 a = __ldcs(reinterpret_cast<const uint4*>(p));
+        const uint4 b = __ldcs(reinterpret_cast<const uint4*>(p + 16));
         const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
         for (int j = 0; j < 16; ++j) x[j] = static_cast<int16_t>((w[j >> 1] >> (16 * (j & 1))) & 0xFFFF);
@@ -121,19 +74,32 @@ __device__ __forceinline__ void store_row(uint8_t* p, int elem, const int (&v)[1
         uint32_t w[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            w[q] = (v[4 * q] & 0xFF) | ((v[4 * q + 1] & 0xFF) << 8) | ((v[4 * q + 2] & 0xFF) << 16) |
-                   (static_cast<uint32_t>(v[4 * q + 3] & 0xFF) << 24);
-        *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+            w[q] = __byte_perm(__byte_perm(v[4 * q], v[4 * q + 1], 0x0040), __byte_perm(v[4 * q + 2], v[4 * q + 3], 0x0040),
+                               0x5410);
+        __stcs(reinterpret_cast<uint4*>(p), make_uint4(w[0], w[1], w[2], w[3]));
     } else {
         uint32_t w[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) w[q] = (v[2 * q] & 0xFFFF) | (static_cast<uint32_t>(v[2 * q + 1] & 0xFFFF) << 16);
-        *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
-        *reinterpret_cast<uint4*>(p + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+        for (int q = 0; q < 8; ++q) w[q] = __byte_perm(v[2 * q], v[2 * q + 1], 0x5410);
+        __stcs(reinterpret_cast<uint4*>(p), make_uint4(w[0], w[1], w[2], w[3]));
+        __stcs(reinterpret_cast<uint4*>(p + 16), make_uint4(w[4], w[5], w[6], w[7]));
     }
 }
 
-constexpr int kBlkPerCta = 8;  // 16 threads per block, 128 threads per CTA
+// 64-bit block index -> byte offset of its top-left pixel and image index
+__device__ __forceinline__ long long block_offset(long long b, const Geom& g, int* n_out, int* row0_out) {
+    const long long per_img = static_cast<long long>(g.BY) * g.BX;
+    const int n = static_cast<int>(b / per_img);
+    const int rem = static_cast<int>(b - n * per_img);
+    const int by = rem / g.BX;
+    const int bx = rem - by * g.BX;
+    *n_out = n;
+    *row0_out = by * 16;
+    return n * g.istride + static_cast<long long>(by * 16) * g.pitch + bx * 16LL * g.elem;
+}
+
+constexpr int kBlkPerCta = 8;   // standalone inverse: 16 threads per block
+
 }  // namespace
 
 // ------------------------------------------------------------------ K5
@@ -146,13 +112,13 @@ __global__ void __launch_bounds__(128) inverse_kernel(const int32_t* __restrict_
     const long long b = static_cast<long long>(blockIdx.x) * kBlkPerCta + sub;
     const bool valid = b < g.nblocks;
     if (valid) {
-        // column t of the coefficient block: c_k = weight(k, t)·qcoef[k][t]
+        // column t of the level block, weighted: c_k = weight(k, t)·qcoef[k][t]
         V c[16], u[16];
         const int32_t* blk = qcoef + b * 256;
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
             const int32_t q = blk[k * 16 + t];
-            if constexpr (UNIFORM) c[k] = static_cast<double>(step) * static_cast<double>(q) * inv_sqrt_G(k, t);
+            if constexpr (UNIFORM) c[k] = static_cast<double>(step) * static_cast<double>(q) * (s_of(k) * s_of(t));
             else c[k] = q * w_of(k, t);
         }
         net_inv(c, u);   // Tᵀ applied down the column
@@ -172,69 +138,145 @@ __global__ void __launch_bounds__(128) inverse_kernel(const int32_t* __restrict_
         if constexpr (UNIFORM) pix[j] = uniform_pixel(a[j], maxpix);
         else pix[j] = zonal_pixel(a[j], maxpix);
     }
-    const BlkAddr ad = block_addr(b, g);
-    store_row(recon + ad.img_off + static_cast<long long>(t) * g.pitch, g.elem, pix);
+    int n, row0;
+    const long long off = block_offset(b, g, &n, &row0);
+    store_row(recon + off + static_cast<long long>(t) * g.pitch, g.elem, pix);
 }
 
 // ------------------------------------------------------- fused codec (K2/K3)
+struct CodecParams {
+    int PX;                  // block pairs per strip = ceil(BX / 2)
+    long long n_pairs;       // N·BY·PX
+    long long chunk;         // pairs per CTA
+    int r, step;
+};
+
 template <bool UNIFORM>
-__global__ void __launch_bounds__(128) codec_kernel(const uint8_t* __restrict__ src, uint8_t* recon,
-                                                    unsigned long long* sse, const Geom g, int r, int step) {
+struct CodecCfg {
+    static constexpr int kWarps = UNIFORM ? 4 : 8;   // static smem < 48 KB per CTA
+};
+
+template <bool UNIFORM>
+__global__ void __launch_bounds__(CodecCfg<UNIFORM>::kWarps * 32) codec_kernel(const uint8_t* __restrict__ src, uint8_t* recon,
+                                                                 unsigned long long* sse, const Geom g,
+                                                                 const CodecParams cp) {
     using V = typename std::conditional<UNIFORM, double, int32_t>::type;
-    __shared__ int32_t sy[kBlkPerCta][16][17];
-    __shared__ V su[kBlkPerCta][16][17];
-    const int sub = threadIdx.x >> 4, t = threadIdx.x & 15;
-    const long long b = static_cast<long long>(blockIdx.x) * kBlkPerCta + sub;
-    const bool valid = b < g.nblocks;
-    BlkAddr ad{};
-    int32_t x[16];
-    if (valid) {
-        ad = block_addr(b, g);
-        load_row(src + ad.img_off + static_cast<long long>(t) * g.pitch, g.elem, x);
-        int32_t y[16];
-        net_fwd(x, y);   // row t of X·Tᵀ
+    constexpr int kCodecWarps = CodecCfg<UNIFORM>::kWarps;
+    // per warp: forward transposition tile (int32, row pitch 20 words) and
+    // inverse transposition tile (V, row pitch 17); block 1 offset by a bank shift
+    __shared__ __align__(16) int32_t sy[kCodecWarps][2][16 * 20 + 16];
+    __shared__ V su[kCodecWarps][2][16][17];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int h = lane >> 4, t = lane & 15;
+    int32_t* ty = &sy[warp][h][h * 16];
+    V(*tu)[17] = su[warp][h];
+
+    // per-lane constants of column t (lane = column in the column pass)
+    V wcol[16];
+    float ccol[16];
+    uint64_t dcol[16];
 #pragma unroll
-        for (int l = 0; l < 16; ++l) sy[sub][t][l] = y[l];
-    }
-    __syncthreads();
-    if (valid) {
-        int32_t col[16], z[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) col[i] = sy[sub][i][t];
-        net_fwd(col, z);   // column t of Z = T·X·Tᵀ
-        V c[16], u[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            if constexpr (UNIFORM)
-                c[k] = static_cast<double>(step) * static_cast<double>(uniform_level(z[k], k, t, step)) *
-                       inv_sqrt_G(k, t);
-            else c[k] = zigzag_rank(k, t) < r ? z[k] * w_of(k, t) : 0;
+    for (int k = 0; k < 16; ++k) {
+        if constexpr (UNIFORM) {
+            const double s = s_of(k) * s_of(t);
+            wcol[k] = static_cast<double>(cp.step) * s;                        // B̂ = q·Δ·s_k·s_t
+            ccol[k] = static_cast<float>(s / cp.step);                           // 1/(Δ·sqrt(G))
+            dcol[k] = static_cast<uint64_t>(cp.step) * cp.step * (g_of(k) * g_of(t));
+        } else {
+            wcol[k] = zigzag_rank(k, t) < cp.r ? w_of(k, t) : 0;               // W ⊙ M_r
+            ccol[k] = 0.f;
+            dcol[k] = 0;
         }
-        net_inv(c, u);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) su[sub][i][t] = u[i];
     }
-    __syncthreads();
-    if (!valid) return;
-    V rrow[16], a[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) rrow[j] = su[sub][t][j];
-    net_inv(rrow, a);
     const int maxpix = (1 << g.bits) - 1;
-    int pix[16];
-    uint32_t e = 0;
+
+    const long long p0 = static_cast<long long>(blockIdx.x) * cp.chunk;
+    long long p1 = p0 + cp.chunk;
+    if (p1 > cp.n_pairs) p1 = cp.n_pairs;
+    // decode the first pair of this warp; later pairs advance incrementally
+    long long p = p0 + warp;
+    const long long strips = p / cp.PX;
+    int px = static_cast<int>(p - strips * cp.PX);
+    int n = static_cast<int>(strips / g.BY);
+    int by = static_cast<int>(strips - static_cast<long long>(n) * g.BY);
+    int cur_n = n;
+    unsigned long long acc = 0;
+
+    for (; p < p1; p += kCodecWarps) {
+        const int bx = 2 * px + h;
+        const bool valid = bx < g.BX;
+        const long long off = n * g.istride + static_cast<long long>(by * 16 + t) * g.pitch + bx * 16LL * g.elem;
+        if (n != cur_n) {   // image changed (warp-uniform): flush the SSE of the previous one
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        if constexpr (UNIFORM) pix[j] = uniform_pixel(a[j], maxpix);
-        else pix[j] = zonal_pixel(a[j], maxpix);
-        const int d = pix[j] - x[j];
-        e += static_cast<uint32_t>(d * d);
+            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0 && acc) atomicAdd(sse + cur_n, acc);
+            acc = 0;
+            cur_n = n;
+        }
+        // ---- row t of X, row pass of the forward transform: Y = X·Tᵀ
+        int32_t x[16];
+        if (valid) load_row(src + off, g.elem, x);
+        else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) x[j] = 0;
+        }
+        {
+            int32_t y[16];
+            net_fwd(x, y);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                *reinterpret_cast<int4*>(ty + t * 20 + 4 * q) = make_int4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+        }
+        __syncwarp();
+        // ---- column t: Z[:, t] = T·Y[:, t]; quantise; inverse down the column
+        {
+            int32_t col[16], z[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) col[k] = ty[k * 20 + t];
+            net_fwd(col, z);
+            V c[16], u[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                if constexpr (UNIFORM) c[k] = static_cast<double>(uniform_level(z[k], ccol[k], dcol[k])) * wcol[k];
+                else c[k] = z[k] * wcol[k];
+            }
+            net_inv(c, u);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) tu[i][t] = u[i];
+        }
+        __syncwarp();
+        // ---- row t: A′[t, :] = (Tᵀ·B̂)[t, :]·T, round, clamp, SSE, store
+        V rr[16], a[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) rr[j] = tu[t][j];
+        net_inv(rr, a);
+        int pix[16];
+        uint32_t e = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if constexpr (UNIFORM) pix[j] = uniform_pixel(a[j], maxpix);
+            else pix[j] = zonal_pixel(a[j], maxpix);
+            const int d = pix[j] - x[j];
+            e += static_cast<uint32_t>(d * d);
+        }
+        if (valid) {
+            if (by * 16 + t < g.VH) acc += e;
+            if (recon) store_row(recon + off, g.elem, pix);
+        }
+        __syncwarp();
+        // next pair of this warp
+        px += kCodecWarps;
+        while (px >= cp.PX) {
+            px -= cp.PX;
+            if (++by == g.BY) {
+                by = 0;
+                ++n;
+            }
+        }
     }
-    if (ad.row0 + t >= g.VH) e = 0;   // rows beyond valid_height do not count
-    if (recon) store_row(recon + ad.img_off + static_cast<long long>(t) * g.pitch, g.elem, pix);
 #pragma unroll
-    for (int o = 8; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-    if (t == 0 && e) atomicAdd(sse + ad.n, static_cast<unsigned long long>(e));
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0 && acc) atomicAdd(sse + cur_n, acc);
 }
 
 // ------------------------------------------------------------------ K6
@@ -298,7 +340,6 @@ int finish_psnr(const Geom& g, uint64_t* sse, double* psnr, cudaStream_t st) {
                                                   peak * peak * P);
     return static_cast<int>(cudaGetLastError());
 }
-
 }  // namespace
 
 int launch_quantize(const int32_t* coef, const Geom& g, const dct16a_quant& q, int32_t* qcoef,
@@ -336,20 +377,35 @@ int launch_psnr(const void* ref, const void* test, const Geom& g, uint64_t* sse,
     return finish_psnr(g, sse, psnr, st);
 }
 
+int launch_codec_generic(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse,
+                         cudaStream_t st) {
+    CodecParams cp;
+    cp.PX = (g.BX + 1) / 2;
+    cp.n_pairs = static_cast<long long>(g.N) * g.BY * cp.PX;
+    const int warps = q.mode == DCT16A_UNIFORM ? CodecCfg<true>::kWarps : CodecCfg<false>::kWarps;
+    const int ctas_per_sm = 16 / warps;
+    long long grid = static_cast<long long>(num_sms()) * ctas_per_sm;
+    const long long min_chunk = 4 * warps;
+    if (grid * min_chunk > cp.n_pairs) grid = (cp.n_pairs + min_chunk - 1) / min_chunk;
+    cp.chunk = (cp.n_pairs + grid - 1) / grid;
+    cp.r = q.r;
+    cp.step = q.step;
+    auto* s = reinterpret_cast<unsigned long long*>(sse);
+    if (q.mode == DCT16A_UNIFORM)
+        codec_kernel<true><<<static_cast<unsigned>(grid), warps * 32, 0, st>>>(
+            static_cast<const uint8_t*>(src), static_cast<uint8_t*>(recon), s, g, cp);
+    else
+        codec_kernel<false><<<static_cast<unsigned>(grid), warps * 32, 0, st>>>(
+            static_cast<const uint8_t*>(src), static_cast<uint8_t*>(recon), s, g, cp);
+    return static_cast<int>(cudaGetLastError());
+}
+
 int launch_codec(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse,
                  double* psnr, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(uint64_t) * g.N, st);
     if (e) return static_cast<int>(e);
-    const long long grid = (g.nblocks + kBlkPerCta - 1) / kBlkPerCta;
-    auto* s = reinterpret_cast<unsigned long long*>(sse);
-    if (q.mode == DCT16A_UNIFORM)
-        codec_kernel<true><<<static_cast<unsigned>(grid), 128, 0, st>>>(
-            static_cast<const uint8_t*>(src), static_cast<uint8_t*>(recon), s, g, q.r, q.step);
-    else
-        codec_kernel<false><<<static_cast<unsigned>(grid), 128, 0, st>>>(
-            static_cast<const uint8_t*>(src), static_cast<uint8_t*>(recon), s, g, q.r, q.step);
-    e = cudaGetLastError();
-    if (e) return static_cast<int>(e);
+    int rc = launch_codec_generic(src, g, q, recon, sse, st);
+    if (rc) return rc;
     return finish_psnr(g, sse, psnr, st);
 }
 

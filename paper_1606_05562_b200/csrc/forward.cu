@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(FwdCfg<ELEM, SM>::kWarps * 32, FwdCfg<ELEM, SM
     const int px = lane * 16;
     const int lane_off = (px / p.box_w) * 16 * p.box_w * ELEM + (px % p.box_w) * ELEM;
     const int row_pitch = p.box_w * ELEM;
+    const int box_b = p.BX < kTile ? p.BX : kTile;   // blocks per output box (dim 1)
     int obuf = 0;
     int it = 0;
     for (long long tix = gw; tix < p.n_tiles; tix += nw, ++it) {
@@ -225,17 +226,20 @@ __global__ void __launch_bounds__(FwdCfg<ELEM, SM>::kWarps * 32, FwdCfg<ELEM, SM
                 if (lane == 0) bulk_wait_read<SC::kBufs - 1>();
             }
             __syncwarp();
-            uint8_t* buf = outb + obuf * SC::kBytes + half * (kTile * 128);
-            uint8_t* ob = buf + lane * 128;
-            const int sw = lane & 7;
+            uint8_t* buf = outb + obuf * SC::kBytes;
+            // staging row of this lane inside the TMA box {32 ints, box_b blocks, kPairs}
+            uint8_t* ob = buf + (half * box_b + lane) * 128;
+            const int sw = (smem_addr(ob) >> 7) & 7;   // 128-byte swizzle: chunk ^= row & 7
+            if (SM == 2 || lane < box_b) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-                *reinterpret_cast<int4*>(ob + ((c ^ sw) << 4)) =
-                    make_int4(z0[4 * c], z0[4 * c + 1], z0[4 * c + 2], z0[4 * c + 3]);
+                for (int c = 0; c < 4; ++c)
+                    *reinterpret_cast<int4*>(ob + ((c ^ sw) << 4)) =
+                        make_int4(z0[4 * c], z0[4 * c + 1], z0[4 * c + 2], z0[4 * c + 3]);
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-                *reinterpret_cast<int4*>(ob + (((c + 4) ^ sw) << 4)) =
-                    make_int4(z1[4 * c], z1[4 * c + 1], z1[4 * c + 2], z1[4 * c + 3]);
+                for (int c = 0; c < 4; ++c)
+                    *reinterpret_cast<int4*>(ob + (((c + 4) ^ sw) << 4)) =
+                        make_int4(z1[4 * c], z1[4 * c + 1], z1[4 * c + 2], z1[4 * c + 3]);
+            }
             if constexpr (SM == 2) {
                 __syncwarp();
                 // lanes 8j..8j+7 move the 128 B row pair of block 4i+j: one warp
@@ -252,7 +256,7 @@ __global__ void __launch_bounds__(FwdCfg<ELEM, SM>::kWarps * 32, FwdCfg<ELEM, SM
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    tma_store_4d(&tout, buf - half * (kTile * 128), 0, bx0, r - half,
+                    tma_store_4d(&tout, buf, 0, bx0, r - half,
                                  static_cast<int32_t>(strip));
                     bulk_commit();
                 }
