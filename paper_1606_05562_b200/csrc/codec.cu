@@ -13,6 +13,7 @@
 // once per thread.
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <type_traits>
 
@@ -400,11 +401,22 @@ int launch_codec_generic(const void* src, const Geom& g, const dct16a_quant& q, 
     return static_cast<int>(cudaGetLastError());
 }
 
+// DCT16A_CODEC_PATH=1 forces the generic kernel (tests compare both paths)
+static int codec_path() {
+    static int m = [] {
+        const char* e = getenv("DCT16A_CODEC_PATH");
+        return e ? atoi(e) : 0;
+    }();
+    return m;
+}
+
 int launch_codec(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse,
                  double* psnr, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(uint64_t) * g.N, st);
     if (e) return static_cast<int>(e);
-    int rc = launch_codec_generic(src, g, q, recon, sse, st);
+    int rc = 1;
+    if (q.mode == DCT16A_ZONAL && codec_path() != 1) rc = launch_zonal_tpb(src, g, q.r, recon, sse, st);
+    if (rc == 1) rc = launch_codec_generic(src, g, q, recon, sse, st);
     if (rc) return rc;
     return finish_psnr(g, sse, psnr, st);
 }

@@ -194,10 +194,19 @@ def test_codec_config1():
     _codec_check(synth.image_u8(0)[None], "zonal", 8, r=16)
 
 
-@pytest.mark.parametrize("r", [1, 32, 100, 256])
+@pytest.mark.parametrize("r", [1, 2, 10, 11, 16, 21, 22, 32, 36, 37, 100, 256])
 def test_codec_zonal_varied(r):
+    # r <= 36 runs the thread-per-block kernel (bands 3/5/7), larger r the generic one
     imgs = np.concatenate([synth.batch_u8([40, 41], 48, 272), synth.adversarial_u8(48, 272)])
     _codec_check(imgs, "zonal", 8, r=r)
+
+
+@pytest.mark.parametrize("shape", [(1, 16, 16), (3, 32, 48), (2, 64, 1920), (1, 48, 784)])
+def test_codec_zonal_shapes(shape):
+    n, h, w = shape
+    imgs = synth.batch_u8(range(60, 60 + n), h, w)
+    for r in (16, 32):
+        _codec_check(imgs, "zonal", 8, r=r)
 
 
 def test_codec_zonal_padded_valid_height():
