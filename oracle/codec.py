@@ -167,8 +167,10 @@ def uniform_recon_float(q: np.ndarray, step: int) -> np.ndarray:
     return C_HAT.T @ (step * q).astype(np.float64) @ C_HAT
 
 
-def _uniform_pixel_decimal(qb: np.ndarray, i: int, j: int, step: int) -> decimal.Decimal:
-    ctx = decimal.Context(prec=50)
+def _uniform_pixel_decimal(qb: np.ndarray, i: int, j: int, step: int, prec: int = 50) -> decimal.Decimal:
+    """A′[i][j] = Σ_kl T_ki·T_lj·Δ·q_kl/sqrt(g_k g_l) evaluated term by term
+    with `decimal` at `prec` digits (an independent check of the inverse)."""
+    ctx = decimal.Context(prec=prec)
     acc = decimal.Decimal(0)
     for k in range(B):
         for l in range(B):
@@ -183,21 +185,91 @@ def round_half_away_float(a: np.ndarray) -> np.ndarray:
     return np.sign(a) * np.floor(np.abs(a) + 0.5)
 
 
+# Exact form of the uniform reconstruction (reading A10).  Each weight
+# 144·s_k·s_l = 144/sqrt(G), G = g_k·g_l (S of PAPER.md:315-329), is written as
+# an integer times sqrt(d) with d square-free: sqrt(G) = a·sqrt(d) gives
+# 144/sqrt(G) = (144/(a·d))·sqrt(d).  Then
+#     144·A′/Δ = Σ_d sqrt(d) · J_d,   J_d = Tᵀ·(K_d ⊙ q)·T   (exact integers),
+# with K_d[k][l] = 144/(a·d) where the cell's square-free part is d, else 0.
+def _squarefree_split(G: int) -> tuple[int, int]:
+    """sqrt(G) = a·sqrt(d), d square-free (G > 0)."""
+    a, d = 1, G
+    f = 2
+    while f * f <= d:
+        while d % (f * f) == 0:
+            d //= f * f
+            a *= f
+        f += 1
+    return a, d
+
+
+SQRT_BASIS = (1, 2, 3, 6)
+
+
+def _basis_weights() -> dict:
+    K = {d: np.zeros((B, B), dtype=np.int64) for d in SQRT_BASIS}
+    for k in range(B):
+        for l in range(B):
+            a, d = _squarefree_split(int(GG[k, l]))
+            assert 144 % (a * d) == 0
+            K[d][k, l] = 144 // (a * d)
+    return K
+
+
+K_BASIS = _basis_weights()
+
+
+def uniform_recon_components(q: np.ndarray) -> dict:
+    """J_d = Tᵀ·(K_d ⊙ q)·T for d in (1, 2, 3, 6): 144·A′/Δ = Σ_d sqrt(d)·J_d
+    exactly (int64; dense products of PAPER.md:896-901 with Ĉ = S·T)."""
+    return {d: _integral(T_F.T @ (K_BASIS[d] * q).astype(np.float64) @ T_F) for d in SQRT_BASIS}
+
+
+def round_half_away_exact_uniform(J: dict, step: int, idx: tuple) -> int:
+    """round_half_away(A′) for one pixel from its exact components (reading
+    A6/A10).  If the irrational parts vanish the value is the rational
+    Δ·J_1/144 and is rounded exactly (ties away from zero).  Otherwise A′ is
+    irrational, so it is not a tie, and a 60-digit evaluation decides; the
+    distance of such a value to a half-integer is bounded below by the norm of
+    a non-zero algebraic integer of Q(√2, √3) over its conjugates (> 1e-40
+    here), far above the 1e-55 evaluation error."""
+    j = {d: int(J[d][idx]) for d in SQRT_BASIS}
+    if j[2] == 0 and j[3] == 0 and j[6] == 0:
+        return int(round_half_away_rational(np.array([step * j[1]]), 144)[0])
+    ctx = decimal.Context(prec=60)
+    v = decimal.Decimal(0)
+    for d in SQRT_BASIS:
+        v = ctx.add(v, ctx.multiply(decimal.Decimal(j[d]), ctx.sqrt(decimal.Decimal(d))))
+    v = ctx.divide(ctx.multiply(v, decimal.Decimal(step)), decimal.Decimal(144))
+    frac = abs(v) - abs(v).to_integral_value(rounding=decimal.ROUND_FLOOR)
+    assert abs(frac - decimal.Decimal("0.5")) > decimal.Decimal("1e-40")
+    return int(v.to_integral_value(rounding=decimal.ROUND_HALF_UP))
+
+
 def uniform_codec(X: np.ndarray, step: int, bit_depth: int = 10) -> dict:
-    """Forward, exact uniform q, float64 reconstruction (reading A10) with a
-    50-digit re-evaluation of any pixel within 1e-9 of a .5 boundary."""
+    """Forward, exact uniform q, then the inverse stage of uniform_inverse_levels
+    (float64 reconstruction, reading A10, exact decisions near ties)."""
     Z = forward(X)
     q = uniform_q(Z, step)
+    inv = uniform_inverse_levels(q, step, bit_depth)
+    return {"Z": Z, "q": q, "scaled": scaled_2d(X), "recon": inv["recon"], "n_near_ties": inv["n_near_ties"]}
+
+
+def uniform_inverse_levels(q: np.ndarray, step: int, bit_depth: int = 10) -> dict:
+    """The inverse stage on levels q (..., 16, 16): A′ = Ĉᵀ·(Δq)·Ĉ in float64
+    (PAPER.md:896-901), round half away and clamp (reading A6).  Any pixel
+    within 1e-9 of a .5 boundary (the float64 dense product errs by < 1e-11)
+    is decided exactly from its components J_d (round_half_away_exact_uniform)."""
+    q = np.asarray(q, dtype=np.int64)
     A = uniform_recon_float(q, step)
     frac = np.abs(A) - np.floor(np.abs(A))
     near = np.argwhere(np.abs(frac - 0.5) < 1e-9)
     rec = round_half_away_float(A)
-    for idx in near:
-        *blk, i, j = (int(v) for v in idx)
-        d = _uniform_pixel_decimal(q[tuple(blk)], i, j, step)
-        rec[tuple(idx)] = float(d.to_integral_value(rounding=decimal.ROUND_HALF_UP))
-    recon = clamp_pixels(rec.astype(np.int64), bit_depth)
-    return {"Z": Z, "q": q, "scaled": scaled_2d(X), "recon": recon, "n_near_ties": len(near)}
+    if len(near):
+        J = uniform_recon_components(q)
+        for idx in near:
+            rec[tuple(int(v) for v in idx)] = round_half_away_exact_uniform(J, step, tuple(int(v) for v in idx))
+    return {"A": A, "recon": clamp_pixels(rec.astype(np.int64), bit_depth), "n_near_ties": len(near)}
 
 
 # ------------------------------------------------------- SSE / PSNR (§4)

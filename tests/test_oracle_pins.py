@@ -356,3 +356,90 @@ def test_psnr_closed_forms():
     c = a.copy()
     c[0, 12:, :] = 9
     assert oc.sse(a, c, valid_height=12) == [0]
+
+
+# ------------------------------------- uniform reconstruction, exact decisions
+def _fraction_recon(qb, step):
+    """A′ = Σ_kl T_ki·T_lj·Δ·q_kl/sqrt(g_k g_l) with Fractions, valid when every
+    non-zero q_kl sits in a rational cell (g_k g_l a perfect square)."""
+    T = tr.build_T()
+    g = np.diag(T @ T.T)
+    A = [[Fraction(0)] * 16 for _ in range(16)]
+    for k in range(16):
+        for l in range(16):
+            if qb[k][l] == 0:
+                continue
+            G = int(g[k] * g[l])
+            r = math.isqrt(G)
+            assert r * r == G
+            c = Fraction(step * int(qb[k][l]), r)
+            for i in range(16):
+                for j in range(16):
+                    A[i][j] += c * int(T[k, i]) * int(T[l, j])
+    return A
+
+
+def _round_half_away_fraction(v):
+    m = math.floor(abs(v) + Fraction(1, 2))
+    return m if v >= 0 else -m
+
+
+def test_uniform_components_equal_float_definition():
+    """144·A′/Δ = Σ_d sqrt(d)·J_d (exact components) against the float64 dense
+    definition Ĉᵀ·(Δq)·Ĉ on random levels."""
+    rng = np.random.default_rng(21)
+    q = rng.integers(-300, 301, size=(20, 16, 16))
+    for step in (1, 7, 16):
+        J = oc.uniform_recon_components(q)
+        val = sum(math.sqrt(d) * J[d].astype(np.float64) for d in oc.SQRT_BASIS) * step / 144.0
+        assert np.max(np.abs(val - oc.uniform_recon_float(q, step))) < 1e-9
+
+
+@pytest.mark.parametrize("case", ["flat_dc", "bb_cell", "random_rational"])
+def test_uniform_recon_exact_ties_rational_cells(case):
+    """Exact .5 ties of the reconstruction (possible only when the irrational
+    parts cancel) round away from zero: checked against Fractions."""
+    T = tr.build_T()
+    g = np.diag(T @ T.T)
+    rational = np.array([[math.isqrt(int(g[k] * g[l])) ** 2 == g[k] * g[l] for l in range(16)] for k in range(16)])
+    if case == "flat_dc":           # Δ=24, q00=1: A′ = 24/16 = 1.5 everywhere -> 2
+        step, qb = 24, np.zeros((1, 16, 16), dtype=np.int64)
+        qb[0, 0, 0] = 1
+    elif case == "bb_cell":         # Δ=6, q00=8, q22=1: A′ = 3 ± 1/2 at T_2i·T_2j = ±1
+        step, qb = 6, np.zeros((1, 16, 16), dtype=np.int64)
+        qb[0, 0, 0], qb[0, 2, 2] = 8, 1
+    else:
+        step = 6
+        rng = np.random.default_rng(4)
+        qb = rng.integers(-3, 4, size=(6, 16, 16)) * rational
+        qb[:, 0, 0] = rng.integers(20, 60, size=6)
+    out = oc.uniform_inverse_levels(qb, step, bit_depth=10)
+    n_ties = 0
+    for b in range(qb.shape[0]):
+        A = _fraction_recon(qb[b], step)
+        for i in range(16):
+            for j in range(16):
+                n_ties += (A[i][j] - math.floor(A[i][j])) == Fraction(1, 2)
+                want = min(1023, max(0, _round_half_away_fraction(A[i][j])))
+                assert out["recon"][b, i, j] == want, (b, i, j, A[i][j])
+    assert n_ties > 0
+    if case != "flat_dc":
+        assert out["n_near_ties"] > 0
+
+
+def test_uniform_recon_near_ties_irrational_vs_decimal():
+    """Pixels whose float64 value lies within 1e-3 of a .5 boundary, with
+    irrational parts, against a 80-digit evaluation of the dense definition."""
+    rng = np.random.default_rng(13)
+    q = rng.integers(-2, 3, size=(400, 16, 16))
+    q[:, 0, 0] = rng.integers(30, 90, size=400)
+    step = 16
+    out = oc.uniform_inverse_levels(q, step, bit_depth=10)
+    A = out["A"]
+    frac = np.abs(A) - np.floor(np.abs(A))
+    idx = np.argwhere(np.abs(frac - 0.5) < 1e-3)
+    assert len(idx) >= 5
+    for b, i, j in idx[:40]:
+        d = oc._uniform_pixel_decimal(q[b], int(i), int(j), step, prec=80)
+        want = int(d.to_integral_value(rounding=decimal.ROUND_HALF_UP))
+        assert out["recon"][b, i, j] == min(1023, max(0, want))
