@@ -143,6 +143,23 @@ DCT16A_API int dct16a_codec(const void* src, const dct16a_desc* desc,
                             const dct16a_quant* quant, void* recon,
                             uint64_t* sse, double* psnr, void* stream);
 
+/*
+ * dct16a_set_option / dct16a_get_option — process-wide knobs for tuning and
+ * cross-checking; they never change results (every kernel choice computes the
+ * same bytes).  Initial values come from the environment variables named
+ * below; set_option returns DCT16A_EDOMAIN for an unknown option or value.
+ *   DCT16A_OPT_CODEC_PATH (env DCT16A_CODEC_PATH): fused-codec kernel choice,
+ *     0 = automatic (default): zonal 8-bit with r <= 36 on the thread-per-block
+ *         kernel, everything else on the warp-per-block-pair kernel;
+ *     1 = zonal on the generic kernel; 2 = always the warp-per-block-pair kernel.
+ *   DCT16A_OPT_FWD_STORE (env DCT16A_FWD_STORE): output path of the forward
+ *     kernel, -1 = default, 0..5 = the variants of profiles/r01_fwd_store_modes.md.
+ */
+#define DCT16A_OPT_CODEC_PATH 1
+#define DCT16A_OPT_FWD_STORE  2
+DCT16A_API int dct16a_set_option(int option, int value);
+DCT16A_API int dct16a_get_option(int option);
+
 /* Thread-local description of the calling thread's last failure ("" if none). */
 DCT16A_API const char* dct16a_last_error(void);
 

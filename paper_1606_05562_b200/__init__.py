@@ -8,9 +8,10 @@ memory, streams and process groups only.
 """
 from __future__ import annotations
 
-from ._lib import (UNIFORM, ZONAL, Dct16aError, Desc, Quant, dct16a_codec, dct16a_forward,  # noqa: F401
-                   dct16a_inverse, dct16a_last_error, dct16a_psnr, dct16a_quantize, dct16a_version,
-                   desc_of, lib, make_desc, make_quant)
+from ._lib import (OPT_CODEC_PATH, OPT_FWD_STORE, UNIFORM, ZONAL, Dct16aError, Desc, Quant,  # noqa: F401
+                   dct16a_codec, dct16a_forward, dct16a_get_option, dct16a_inverse, dct16a_last_error,
+                   dct16a_psnr, dct16a_quantize, dct16a_set_option, dct16a_version, desc_of, lib,
+                   make_desc, make_quant)
 
 __version__ = "0.1.0"
 

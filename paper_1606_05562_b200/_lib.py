@@ -15,6 +15,8 @@ LIB_PATH = os.path.join(PKG, "libdct16a.so")
 
 ZONAL = 0
 UNIFORM = 1
+OPT_CODEC_PATH = 1
+OPT_FWD_STORE = 2
 
 ERRORS = {-1: "ENULL", -2: "ESHAPE", -3: "EPITCH", -4: "EALIGN", -5: "EDOMAIN", -6: "ECUDA"}
 
@@ -56,6 +58,10 @@ def lib() -> ctypes.CDLL:
         L.dct16a_codec.argtypes = [vp, P(Desc), P(Quant), vp, vp, vp, vp]
         for f in ("dct16a_forward", "dct16a_quantize", "dct16a_inverse", "dct16a_psnr", "dct16a_codec"):
             getattr(L, f).restype = ctypes.c_int
+        L.dct16a_set_option.argtypes = [ctypes.c_int, ctypes.c_int]
+        L.dct16a_set_option.restype = ctypes.c_int
+        L.dct16a_get_option.argtypes = [ctypes.c_int]
+        L.dct16a_get_option.restype = ctypes.c_int
         L.dct16a_last_error.restype = ctypes.c_char_p
         L.dct16a_version.restype = ctypes.c_char_p
         _lib = L
@@ -144,3 +150,14 @@ def dct16a_version() -> str:
 
 def dct16a_last_error() -> str:
     return lib().dct16a_last_error().decode()
+
+
+def dct16a_set_option(option: int, value: int) -> None:
+    _check(lib().dct16a_set_option(option, value))
+
+
+def dct16a_get_option(option: int) -> int:
+    v = lib().dct16a_get_option(option)
+    if option not in (OPT_CODEC_PATH, OPT_FWD_STORE):
+        _check(v)
+    return v

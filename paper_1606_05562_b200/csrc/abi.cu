@@ -7,7 +7,9 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <atomic>
 #include <mutex>
+#include <stdlib.h>
 
 #include "internal.h"
 
@@ -127,6 +129,21 @@ int encode_tiled(CUtensorMap* map, CUtensorMapDataType dt, uint32_t rank, const 
     return static_cast<int>(r);
 }
 
+namespace {
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+std::atomic<int> g_codec_path{env_int("DCT16A_CODEC_PATH", 0)};
+std::atomic<int> g_fwd_store{env_int("DCT16A_FWD_STORE", -1)};
+}  // namespace
+
+int get_option(int option) {
+    if (option == DCT16A_OPT_CODEC_PATH) return g_codec_path.load(std::memory_order_relaxed);
+    if (option == DCT16A_OPT_FWD_STORE) return g_fwd_store.load(std::memory_order_relaxed);
+    return 0;
+}
+
 int num_sms() {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -198,6 +215,26 @@ DCT16A_API int dct16a_codec(const void* src, const dct16a_desc* desc, const dct1
     if (psnr && (reinterpret_cast<uintptr_t>(psnr) & 7u)) return fail(DCT16A_EALIGN, "psnr not 8-byte aligned");
     return launched(launch_codec(src, g, *quant, recon, sse, psnr, static_cast<cudaStream_t>(stream)),
                     "dct16a_codec");
+}
+
+DCT16A_API int dct16a_set_option(int option, int value) {
+    if (option == DCT16A_OPT_CODEC_PATH) {
+        if (value < 0 || value > 2) return fail(DCT16A_EDOMAIN, "codec path %d not in [0, 2]", value);
+        g_codec_path.store(value);
+        return DCT16A_OK;
+    }
+    if (option == DCT16A_OPT_FWD_STORE) {
+        if (value < -1 || value > 5) return fail(DCT16A_EDOMAIN, "forward store mode %d not in [-1, 5]", value);
+        g_fwd_store.store(value);
+        return DCT16A_OK;
+    }
+    return fail(DCT16A_EDOMAIN, "unknown option %d", option);
+}
+
+DCT16A_API int dct16a_get_option(int option) {
+    if (option != DCT16A_OPT_CODEC_PATH && option != DCT16A_OPT_FWD_STORE)
+        return fail(DCT16A_EDOMAIN, "unknown option %d", option);
+    return get_option(option);
 }
 
 DCT16A_API const char* dct16a_last_error(void) { return g_err; }

@@ -21,6 +21,7 @@
 #include "net16.cuh"
 #include "quant.cuh"
 #include "tables.cuh"
+#include "uexact.cuh"
 
 namespace dct16a {
 
@@ -134,10 +135,29 @@ __global__ void __launch_bounds__(128) inverse_kernel(const int32_t* __restrict_
     net_inv(rrow, a);    // ... and along row t: A′ = Tᵀ·B̂·T
     const int maxpix = (1 << g.bits) - 1;
     int pix[16];
+    if constexpr (UNIFORM) {
+        // floor(A′ + 1/2) from the float64 value; pixels within 2^-20 of a .5
+        // boundary are decided exactly from the levels (uexact.cuh, reading A10)
+        uint32_t nm = 0;
+        int n0[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        if constexpr (UNIFORM) pix[j] = uniform_pixel(a[j], maxpix);
-        else pix[j] = zonal_pixel(a[j], maxpix);
+        for (int j = 0; j < 16; ++j) {
+            bool nr;
+            pix[j] = round_f64(a[j], nr, n0[j]);
+            nm |= (nr ? 1u : 0u) << j;
+        }
+        if (nm) {
+            int32_t qb[256];
+            for (int i = 0; i < 256; ++i) qb[i] = qcoef[b * 256 + i];
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if ((nm >> j) & 1u) pix[j] = uniform_exact_floor(qb, t, j, step, n0[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pix[j] = min(max(pix[j], 0), maxpix);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pix[j] = zonal_pixel(a[j], maxpix);
     }
     int n, row0;
     const long long off = block_offset(b, g, &n, &row0);
@@ -401,22 +421,23 @@ int launch_codec_generic(const void* src, const Geom& g, const dct16a_quant& q, 
     return static_cast<int>(cudaGetLastError());
 }
 
-// DCT16A_CODEC_PATH=1 forces the generic kernel (tests compare both paths)
-static int codec_path() {
-    static int m = [] {
-        const char* e = getenv("DCT16A_CODEC_PATH");
-        return e ? atoi(e) : 0;
-    }();
-    return m;
-}
-
+// Kernel choice of the fused codec (option DCT16A_OPT_CODEC_PATH, include/dct16a.h):
+//   0 auto: zonal 8-bit with r <= 36 -> thread-per-block kernel (zonal_tpb.cu),
+//           everything else -> warp-per-block-pair kernel (codec_warp.cu);
+//   1: zonal -> the generic kernel above (uniform stays on codec_warp.cu);
+//   2: always codec_warp.cu.
+// The three implementations are independent cross-checks of each other.
 int launch_codec(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse,
                  double* psnr, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(uint64_t) * g.N, st);
     if (e) return static_cast<int>(e);
+    const int path = get_option(DCT16A_OPT_CODEC_PATH);
     int rc = 1;
-    if (q.mode == DCT16A_ZONAL && codec_path() != 1) rc = launch_zonal_tpb(src, g, q.r, recon, sse, st);
-    if (rc == 1) rc = launch_codec_generic(src, g, q, recon, sse, st);
+    if (q.mode == DCT16A_ZONAL && path == 0) rc = launch_zonal_tpb(src, g, q.r, recon, sse, st);
+    if (rc == 1) {
+        if (q.mode == DCT16A_ZONAL && path == 1) rc = launch_codec_generic(src, g, q, recon, sse, st);
+        else rc = launch_codec_warp(src, g, q, recon, sse, st);
+    }
     if (rc) return rc;
     return finish_psnr(g, sse, psnr, st);
 }

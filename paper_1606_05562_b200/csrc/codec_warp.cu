@@ -1,0 +1,489 @@
+// codec_warp.cu — the fused codec with 16 lanes per 16x16 block (one warp holds
+// a block pair): forward, quantisation with S folded in
+// (PAPER.md:305-344), inverse (896-901), round half away / clamp (reading A6),
+// per-image SSE (906-910).  It serves the uniform quantiser (config 4, any bit
+// depth) and the zonal cases the thread-per-block kernel does not cover
+// (10-bit, r > 36).
+//
+// * Data: each warp streams tiles of 8 blocks (16 rows x 128 px) through a
+//   3-stage TMA ring in the 128-byte swizzle, so the lanes of a quarter-warp
+//   (rows 0-7 of one block) read distinct 16-byte chunks with ld.shared.v4;
+//   the reconstruction overwrites the tile in place and leaves by TMA store.
+// * Forward: lane t holds row t, the row pass runs the 60-add network of
+//   Eq. (1) in float32 (exact: every partial sum is an integer < 2^24, V9);
+//   the transposition buffer of the paper is a per-warp
+//   smem tile; lane l then runs the column pass on column l.
+// * Uniform quantiser (reading A9): m = floor(|Z|·c + 1/2 + δ) from one FMA and
+//   one round-down magic add keeping F fraction bits.  δ (> the float error,
+//   below the 1/(2Δ·sqrt(G)) spacing of the rational cells) makes the rational
+//   cells — the only ones with exact ties — exact; in the irrational cells a
+//   value whose fraction falls in the window [0, δ + 2·err) is re-decided
+//   exactly in integers (uniform_fix).
+// * Uniform inverse in float64 (reading A10): the level enters as the double
+//   1.5·2^E + m built from its bits, and one DFMA with the signed weight
+//   Δ·s_k·s_l and the constant −fl(1.5·2^E·w) forms the input (error < 1e-11);
+//   two 60-add networks, smem transposition in between; rounding by one
+//   round-down add (round_f64), pixels within 2^-20 of a .5 boundary are
+//   decided exactly (uniform_exact_floor).
+// * Zonal inverse in float32, exact (half-integers < 2^23): N + 1152.5 on the
+//   DC input, pixel = floor((N + 1152.5)/2304) as in zonal_tpb.cu.
+#include <cuda.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <type_traits>
+
+#include "internal.h"
+#include "net16.cuh"
+#include "ptx.cuh"
+#include "quant.cuh"
+#include "tables.cuh"
+#include "uexact.cuh"
+
+namespace dct16a {
+namespace {
+
+constexpr int kWWarps = 4;    // warps per CTA
+constexpr int kWStages = 3;   // TMA ring depth per warp
+constexpr int kWTile = 8;     // blocks per tile (128 px)
+// per-warp transposition bytes (2 blocks x 16 x 17 doubles = 4352), rounded so
+// that every warp's stages stay 1024-byte aligned (the 128-byte swizzle pattern
+// is taken from smem address bits 7-9)
+constexpr int kWXpose = 5120;
+
+template <int ELEM, bool UNIFORM>
+struct WCfg {
+    static constexpr int kStageBytes = 16 * kWTile * 16 * ELEM;   // 2 KB (u8) / 4 KB (u16)
+    static constexpr int kWarpBytes = kWStages * kStageBytes + kWXpose;
+    static_assert(kWarpBytes % 1024 == 0, "stages must stay 1024-byte aligned");
+    static constexpr int kSmem = 1024 + kWWarps * kWarpBytes + kWWarps * kWStages * 8;
+    static constexpr int kFit = (227 * 1024) / (kSmem + 1024);
+    // the float64 path needs ~170 registers: at most 3 CTAs (12 warps) per SM
+    static constexpr int kCtasPerSm = UNIFORM ? (kFit < 3 ? kFit : 3) : (kFit < 4 ? kFit : 4);
+};
+
+struct WParams {
+    int W, BX, BY, VH, tiles_per_strip, maxpix;
+    long long n_tiles, chunk;
+    int has_recon;
+    // zonal
+    int r;
+    // uniform
+    int step, F, wbits, hi_shift, hi_c;
+    float magic_f, half_delta;
+    uint32_t magic_bits;
+};
+
+__device__ __forceinline__ uint8_t* walign1024(uint8_t* smem_raw) {
+    return smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+}
+
+// byte offset of the 16-byte chunk c of row t in a 128-byte-swizzled box
+__device__ __forceinline__ int swz(int t, int c) { return t * 128 + ((c ^ (t & 7)) << 4); }
+
+template <int ELEM>
+__device__ __forceinline__ void w_tile_coords(const WParams& p, long long tix, int* n, int* by, int* x0) {
+    const long long strip = tix / p.tiles_per_strip;
+    const int tb = static_cast<int>(tix - strip * p.tiles_per_strip);
+    *n = static_cast<int>(strip / p.BY);
+    *by = static_cast<int>(strip - static_cast<long long>(*n) * p.BY);
+    *x0 = tb * kWTile * 16;
+}
+
+template <int ELEM>
+__device__ __forceinline__ void w_issue(const CUtensorMap* tin, const WParams& p, long long tix, uint8_t* stage,
+                                        uint64_t* bar, uint64_t pol) {
+    int n, by, x0;
+    w_tile_coords<ELEM>(p, tix, &n, &by, &x0);
+    constexpr int box_px = 128 / ELEM;
+    const int nbox = (ELEM == 2 && x0 + box_px < p.W) ? 2 : 1;
+    mbar_arrive_expect_tx(bar, static_cast<uint32_t>(nbox * 2048));
+    for (int h = 0; h < nbox; ++h) tma_load_3d(stage + h * 2048, tin, bar, x0 + h * box_px, by * 16, n, pol);
+}
+
+template <int ELEM>
+__device__ __forceinline__ void w_store(const CUtensorMap* tout, const WParams& p, long long tix, uint8_t* stage) {
+    int n, by, x0;
+    w_tile_coords<ELEM>(p, tix, &n, &by, &x0);
+    constexpr int box_px = 128 / ELEM;
+    const int nbox = (ELEM == 2 && x0 + box_px < p.W) ? 2 : 1;
+    for (int h = 0; h < nbox; ++h) tma_store_3d(tout, stage + h * 2048, x0 + h * box_px, by * 16, n);
+}
+
+// smem byte offsets (within the stage) of the 16·ELEM bytes of row t of block bb
+template <int ELEM>
+__device__ __forceinline__ void row_addr(int bb, int t, int* a0, int* a1) {
+    if (ELEM == 1) {
+        *a0 = swz(t, bb);
+        *a1 = *a0;
+    } else {
+        const int base = (bb >> 2) * 2048, c = (bb & 3) * 2;
+        *a0 = base + swz(t, c);
+        *a1 = base + swz(t, c + 1);
+    }
+}
+
+template <int ELEM>
+__device__ __forceinline__ void load_px(const uint8_t* stage, int a0, int a1, uint32_t (&w)[4 * ELEM]) {
+    const uint4 v = *reinterpret_cast<const uint4*>(stage + a0);
+    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+    if (ELEM == 2) {
+        const uint4 u = *reinterpret_cast<const uint4*>(stage + a1);
+        w[4] = u.x; w[5] = u.y; w[6] = u.z; w[7] = u.w;
+    }
+}
+
+// pixel j of a packed row (u8 or u16)
+template <int ELEM>
+__device__ __forceinline__ int px_of(const uint32_t (&w)[4 * ELEM], int j) {
+    return ELEM == 1 ? static_cast<int>((w[j >> 2] >> (8 * (j & 3))) & 0xFFu)
+                     : static_cast<int>((w[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+}
+
+// Exact levels of one block recomputed from its pixels (rare branch): Z by the
+// integer network, then the exact uniform decision (uniform_level/uniform_fix).
+template <int ELEM>
+__device__ __noinline__ void exact_levels_from_stage(const uint8_t* stage, int bb, int step, int32_t* q) {
+    int32_t Y[16][16];
+    for (int t = 0; t < 16; ++t) {
+        int a0, a1;
+        row_addr<ELEM>(bb, t, &a0, &a1);
+        uint32_t w[4 * ELEM];
+        load_px<ELEM>(stage, a0, a1, w);
+        int32_t x[16], y[16];
+        for (int j = 0; j < 16; ++j) x[j] = px_of<ELEM>(w, j);
+        net_fwd(x, y);
+        for (int l = 0; l < 16; ++l) Y[t][l] = y[l];
+    }
+    for (int l = 0; l < 16; ++l) {
+        int32_t c[16], z[16];
+        for (int t = 0; t < 16; ++t) c[t] = Y[t][l];
+        net_fwd(c, z);
+        for (int k = 0; k < 16; ++k) {
+            const uint32_t az = static_cast<uint32_t>(z[k] < 0 ? -z[k] : z[k]);
+            const uint64_t d2g = static_cast<uint64_t>(step) * step * (g_of(k) * g_of(l));
+            const double e = static_cast<double>(az) / (step * sqrt(static_cast<double>(g_of(k) * g_of(l)))) + 0.5;
+            const int32_t m = uniform_fix(az, static_cast<int32_t>(floor(e)), d2g);
+            q[k * 16 + l] = z[k] < 0 ? -m : m;
+        }
+    }
+}
+
+// Exact uniform level for a coefficient whose float estimate m is flagged (rare).
+__device__ __noinline__ int32_t uniform_fix_call(float z, int32_t m, int step, int G) {
+    const uint32_t az = static_cast<uint32_t>(fabsf(z));
+    return uniform_fix(az, m, static_cast<uint64_t>(step) * step * G);
+}
+
+}  // namespace
+
+template <int ELEM, bool UNIFORM>
+__global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
+    codec_warp_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+                      unsigned long long* __restrict__ sse, const WParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = walign1024(smem_raw);
+    using Cfg = WCfg<ELEM, UNIFORM>;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int h = lane >> 4, t = lane & 15;
+    uint8_t* wbase = smem + warp * Cfg::kWarpBytes;
+    uint8_t* xpose = wbase + kWStages * Cfg::kStageBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kWWarps * Cfg::kWarpBytes) + warp * kWStages;
+
+    const long long gw = static_cast<long long>(blockIdx.x) * kWWarps + warp;
+    const long long t0 = gw * p.chunk;
+    long long t1 = t0 + p.chunk;
+    if (t1 > p.n_tiles) t1 = p.n_tiles;
+    const uint64_t pol = policy_evict_first();
+
+    if (lane == 0) {
+        for (int s = 0; s < kWStages; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+        prefetch_tmap(&tin);
+        if (p.has_recon) prefetch_tmap(&tout);
+        for (int s = 0; s < kWStages - 1; ++s)
+            if (t0 + s < t1) w_issue<ELEM>(&tin, p, t0 + s, wbase + s * Cfg::kStageBytes, &bars[s], pol);
+    }
+    __syncwarp();
+
+    // ---- per-lane constants (lane t is column l = t in the column pass)
+    const int l = t;
+    const int cl = uclass(l);
+    float cq[3];          // uniform: 1/(Δ·sqrt(g_k·g_l)) per class of k
+    double wq[3], kq[3];  // uniform: Δ·s_k·s_l and −fl(1.5·2^E·Δ·s_k·s_l)
+    float wz[16];         // zonal: W ⊙ M_r
+    uint32_t irr = 0;     // uniform: k whose cell (k, l) is irrational
+    if constexpr (UNIFORM) {
+        const double sl = s_of(l);
+        const double Kmag = static_cast<double>(3LL << (19 - p.hi_shift));   // 1.5·2^E, E = 20 - hi_shift
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int kk = c == 0 ? 0 : (c == 1 ? 2 : 3);   // representatives of g = 16, 12, 8
+            const double s = s_of(kk) * sl;
+            cq[c] = static_cast<float>(s / p.step);
+            wq[c] = static_cast<double>(p.step) * s;
+            kq[c] = -(Kmag * wq[c]);
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) irr |= (uclass(k) != cl ? 1u : 0u) << k;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) wz[k] = zigzag_rank(k, l) < p.r ? static_cast<float>(w_of(k, l)) : 0.0f;
+    }
+
+    // per-warp transposition tiles: Y (float, row pitch 20, second block shifted 16 banks)
+    // and U (V = double/float, row pitch 17)
+    float* ty = reinterpret_cast<float*>(xpose) + h * (16 * 20 + 16);
+    using V = typename std::conditional<UNIFORM, double, float>::type;
+    V* tu = reinterpret_cast<V*>(xpose) + h * (16 * 17);
+
+    unsigned long long acc = 0;
+    int cur_n = -1;
+    int it = 0;
+    for (long long tix = t0; tix < t1; ++tix, ++it) {
+        const int s = it % kWStages;
+        uint8_t* stage = wbase + s * Cfg::kStageBytes;
+        mbar_wait(&bars[s], (it / kWStages) & 1);
+        int n, by, x0;
+        w_tile_coords<ELEM>(p, tix, &n, &by, &x0);
+        if (n != cur_n) {
+#pragma unroll
+            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0 && acc) atomicAdd(sse + cur_n, acc);
+            acc = 0;
+            cur_n = n;
+        }
+        const int nb = min(kWTile, p.BX - x0 / 16);
+        const bool row_valid = by * 16 + t < p.VH;
+#pragma unroll 1
+        for (int pair = 0; 2 * pair < nb; ++pair) {
+            const int bb = 2 * pair + h;
+            const bool valid = bb < nb;
+            int a0, a1;
+            row_addr<ELEM>(bb, t, &a0, &a1);
+            // ---- row t: Y[t][:] = X[t][:]·Tᵀ
+            {
+                uint32_t w[4 * ELEM];
+                load_px<ELEM>(stage, a0, a1, w);
+                float x[16], y[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) x[j] = static_cast<float>(px_of<ELEM>(w, j));
+                net_fwd(x, y);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    *reinterpret_cast<float4*>(ty + t * 20 + 4 * q) = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+            }
+            __syncwarp();
+            // ---- column l: Z[:, l] = T·Y[:, l]
+            float z[16];
+            {
+                float col[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) col[k] = ty[k * 20 + l];
+                net_fwd(col, z);
+            }
+            __syncwarp();
+            // ---- quantise, weight, inverse down the column
+            {
+                V c[16], u[16];
+                if constexpr (UNIFORM) {
+                    int32_t m[16];
+                    uint32_t nm = 0;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const float e = fmaf(fabsf(z[k]), cq[uclass(k)], p.half_delta);
+                        const uint32_t v = __float_as_uint(__fadd_rd(e, p.magic_f)) - p.magic_bits;
+                        m[k] = static_cast<int32_t>(v >> p.F);
+                        nm |= ((v & ((1u << p.F) - 1u)) < static_cast<uint32_t>(p.wbits) ? 1u : 0u) << k;
+                    }
+                    nm &= irr;
+                    if (__any_sync(0xffffffffu, nm)) {
+#pragma unroll
+                        for (int k = 0; k < 16; ++k)
+                            if ((nm >> k) & 1u) m[k] = uniform_fix_call(z[k], m[k], p.step, g_of(k) * g_of(l));
+                    }
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const uint32_t sg = __float_as_uint(z[k]) & 0x80000000u;
+                        const double d = __hiloint2double((m[k] << p.hi_shift) + p.hi_c, 0);
+                        const int ck = uclass(k);
+                        const double ws = __hiloint2double(__double2hiint(wq[ck]) ^ static_cast<int>(sg), __double2loint(wq[ck]));
+                        const double ks = __hiloint2double(__double2hiint(kq[ck]) ^ static_cast<int>(sg), __double2loint(kq[ck]));
+                        c[k] = fma(d, ws, ks);
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) c[k] = z[k] * wz[k];
+                    if (l == 0) c[0] += 1152.5f;   // N + 1152.5 everywhere: rounding offset on the DC input
+                }
+                net_inv(c, u);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) tu[i * 17 + l] = u[i];
+            }
+            __syncwarp();
+            // ---- row i = t: A′[i][:] = (Tᵀ·B̂)[i][:]·T, round, clamp
+            int pix[16];
+            {
+                V rr[16], a[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) rr[j] = tu[t * 17 + j];
+                net_inv(rr, a);
+                if constexpr (UNIFORM) {
+                    uint32_t nm = 0;
+                    int n0[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        bool nr;
+                        pix[j] = round_f64(a[j], nr, n0[j]);
+                        nm |= (nr ? 1u : 0u) << j;
+                    }
+                    if (!valid) nm = 0;
+                    if (__any_sync(0xffffffffu, nm)) {
+                        int32_t qb[256];
+                        if (nm) exact_levels_from_stage<ELEM>(stage, bb, p.step, qb);
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if ((nm >> j) & 1u) pix[j] = uniform_exact_floor(qb, t, j, p.step, n0[j]);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) pix[j] = min(max(pix[j], 0), p.maxpix);
+                } else {
+                    const float inv2304 = 1.0f / 2304.0f;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const float tt = fmaxf(a[j] * inv2304, 0.0f);
+                        const uint32_t bits = min(__float_as_uint(__fadd_rd(tt, 8388608.0f)), 0x4B000000u + p.maxpix);
+                        pix[j] = static_cast<int>(bits - 0x4B000000u);
+                    }
+                }
+            }
+            // ---- SSE against the original row, in-place reconstruction
+            {
+                uint32_t w[4 * ELEM];
+                load_px<ELEM>(stage, a0, a1, w);
+                uint32_t e = 0;
+                uint32_t o[4 * ELEM];
+                if (ELEM == 1) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        o[q] = __byte_perm(__byte_perm(pix[4 * q], pix[4 * q + 1], 0x0040),
+                                           __byte_perm(pix[4 * q + 2], pix[4 * q + 3], 0x0040), 0x5410);
+                        const uint32_t d = __vabsdiffu4(o[q], w[q]);
+                        e = __dp4a(d, d, e);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        o[q] = __byte_perm(pix[2 * q], pix[2 * q + 1], 0x5410);
+                        const int d0 = pix[2 * q] - static_cast<int>(w[q] & 0xFFFFu);
+                        const int d1 = pix[2 * q + 1] - static_cast<int>(w[q] >> 16);
+                        e += static_cast<uint32_t>(d0 * d0 + d1 * d1);
+                    }
+                }
+                if (valid && row_valid) acc += e;
+                if (p.has_recon) {
+                    *reinterpret_cast<uint4*>(stage + a0) = make_uint4(o[0], o[1], o[2], o[3]);
+                    if (ELEM == 2) *reinterpret_cast<uint4*>(stage + a1) = make_uint4(o[4], o[5], o[6], o[7]);
+                }
+            }
+            __syncwarp();
+        }
+        if (lane == 0) {
+            if (p.has_recon) {
+                fence_async_smem();
+                w_store<ELEM>(&tout, p, tix, stage);
+                bulk_commit();
+                bulk_wait_read<1>();   // the store of tile tix-1 has left the stage refilled next
+            }
+            const long long nt = tix + kWStages - 1;
+            if (nt < t1) w_issue<ELEM>(&tin, p, nt, wbase + ((it + kWStages - 1) % kWStages) * Cfg::kStageBytes,
+                                       &bars[(it + kWStages - 1) % kWStages], pol);
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+        if (acc) atomicAdd(sse + cur_n, acc);
+        if (p.has_recon) bulk_wait<0>();
+    }
+}
+
+namespace {
+
+template <int ELEM, bool UNIFORM>
+int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse, cudaStream_t st) {
+    using Cfg = WCfg<ELEM, UNIFORM>;
+    CUtensorMap tin, tout;
+    const uint64_t dims[3] = {uint64_t(g.W), uint64_t(g.H), uint64_t(g.N)};
+    const uint64_t strides[2] = {uint64_t(g.pitch), uint64_t(g.istride)};
+    const uint32_t box[3] = {uint32_t(128 / ELEM), 16u, 1u};
+    const CUtensorMapDataType dt = ELEM == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+    if (encode_tiled(&tin, dt, 3, src, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
+        return DCT16A_ECUDA;
+    if (recon) {
+        if (encode_tiled(&tout, dt, 3, recon, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE))
+            return DCT16A_ECUDA;
+    } else {
+        tout = tin;
+    }
+    WParams p{};
+    p.W = g.W;
+    p.BX = g.BX;
+    p.BY = g.BY;
+    p.VH = g.VH;
+    p.tiles_per_strip = (g.BX + kWTile - 1) / kWTile;
+    p.maxpix = (1 << g.bits) - 1;
+    p.n_tiles = static_cast<long long>(g.N) * g.BY * p.tiles_per_strip;
+    p.has_recon = recon != nullptr;
+    p.r = q.r;
+    p.step = q.step;
+    if (UNIFORM) {
+        // e = |Z|/(Δ·sqrt(G)) + 1/2 <= e_max; float error <= e_max·2^-23 (rounded c
+        // and the fma); δ = 2·err keeps the rational cells exact because
+        // δ + err < 1/(32Δ), the smallest spacing of their e (reading A9).
+        const double e_max = 16.0 * p.maxpix / q.step + 1.0;
+        const double err = e_max * 0x1p-23;
+        int nbits = 0;
+        while ((1 << nbits) <= static_cast<int>(e_max) + 1) ++nbits;
+        p.F = 22 - nbits;
+        const float hd = static_cast<float>(0.5 + 2.0 * err);
+        const double delta = static_cast<double>(hd) - 0.5;
+        if (!(delta > err && delta + err < 1.0 / (32.0 * q.step))) return DCT16A_EDOMAIN;
+        p.half_delta = hd;
+        p.magic_f = 1.5f * static_cast<float>(1 << (23 - p.F));
+        memcpy(&p.magic_bits, &p.magic_f, 4);
+        p.wbits = static_cast<int>((delta + 2.0 * err) * (1 << p.F)) + 2;
+        // level -> double 1.5·2^E + m: E with 2^E > 2·m_max, m placed at bit (20 - E) of the high word
+        int E = 1;
+        while ((1 << E) <= 2 * (static_cast<int>(e_max) + 1)) ++E;
+        p.hi_shift = 20 - E;
+        p.hi_c = 0x3FF00000 + ((E) << 20) + (1 << 19);   // high word of 1.5·2^E
+    }
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(codec_warp_kernel<ELEM, UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+        attr = true;
+    }
+    long long warps = static_cast<long long>(num_sms()) * Cfg::kCtasPerSm * kWWarps;
+    if (warps > p.n_tiles) warps = p.n_tiles;
+    p.chunk = (p.n_tiles + warps - 1) / warps;
+    const long long grid = (warps + kWWarps - 1) / kWWarps;
+    codec_warp_kernel<ELEM, UNIFORM><<<static_cast<unsigned>(grid), kWWarps * 32, Cfg::kSmem, st>>>(
+        tin, tout, reinterpret_cast<unsigned long long*>(sse), p);
+    return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace
+
+int launch_codec_warp(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse,
+                      cudaStream_t st) {
+    const bool uni = q.mode == DCT16A_UNIFORM;
+    if (g.elem == 1) return uni ? launch_cw<1, true>(src, g, q, recon, sse, st) : launch_cw<1, false>(src, g, q, recon, sse, st);
+    return uni ? launch_cw<2, true>(src, g, q, recon, sse, st) : launch_cw<2, false>(src, g, q, recon, sse, st);
+}
+
+}  // namespace dct16a

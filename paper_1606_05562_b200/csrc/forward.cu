@@ -313,13 +313,10 @@ int launch_fwd_t(const void* src, const Geom& g, int32_t* coef, cudaStream_t st)
 }
 
 // Output path of the forward kernel.  Default: 16 KB TMA tensor stores (mode 4),
-// measured fastest on config 2; DCT16A_FWD_STORE=0..5 selects
+// measured fastest on config 2; the option DCT16A_OPT_FWD_STORE (include/dct16a.h) selects
 // the other variants for experiments (profiles/r01_fwd_store_modes.md).
 int store_mode(int elem) {
-    static int m = [] {
-        const char* e = getenv("DCT16A_FWD_STORE");
-        return e ? atoi(e) : -1;
-    }();
+    const int m = get_option(DCT16A_OPT_FWD_STORE);
     return m >= 0 ? m : (elem == 1 ? 4 : 0);
 }
 

@@ -40,5 +40,10 @@ int launch_codec(const void* src, const Geom& g, const dct16a_quant& q, void* re
 // thread-per-block zonal codec for 8-bit and small bands; returns 1 if not applicable
 int launch_zonal_tpb(const void* src, const Geom& g, int r, void* recon, uint64_t* sse, cudaStream_t st);
 int zonal_band(int r);
+// warp-per-block-pair codec (uniform, and zonal cases zonal_tpb does not take)
+int launch_codec_warp(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse,
+                      cudaStream_t st);
+// library options (dct16a_set_option); read by the launchers
+int get_option(int option);
 
 }  // namespace dct16a

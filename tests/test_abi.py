@@ -23,7 +23,7 @@ def declared_symbols():
 def test_library_loads_and_exports_header_symbols():
     L = pkg.lib()
     syms = declared_symbols()
-    assert len(syms) == 7
+    assert len(syms) == 9
     for s in syms:
         assert hasattr(L, s), s
     out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
@@ -103,3 +103,18 @@ def test_binding_rejects_cpu_tensors():
     x = torch.zeros((1, 16, 16), dtype=torch.uint8)
     with pytest.raises(ValueError):
         pkg.dct16a_forward(x, torch.zeros((1, 16, 16), dtype=torch.int32))
+
+
+def test_options_validate_and_round_trip():
+    old = pkg.dct16a_get_option(pkg.OPT_CODEC_PATH)
+    for v in (0, 1, 2):
+        pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, v)
+        assert pkg.dct16a_get_option(pkg.OPT_CODEC_PATH) == v
+    pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, old)
+    with pytest.raises(pkg.Dct16aError) as e:
+        pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, 3)
+    assert e.value.code == -5
+    with pytest.raises(pkg.Dct16aError) as e:
+        pkg.dct16a_set_option(99, 0)
+    assert e.value.code == -5
+    assert pkg.dct16a_get_option(pkg.OPT_FWD_STORE) in range(-1, 6)

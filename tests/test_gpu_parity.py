@@ -178,6 +178,17 @@ def test_psnr_kernel():
     assert sse.cpu().tolist() == oc.sse(a, b, 32)
 
 
+@pytest.fixture(params=[0, 1, 2], ids=["auto", "generic", "warp"])
+def codec_path(request):
+    """Every fused-codec test runs on each kernel choice (DCT16A_OPT_CODEC_PATH):
+    the thread-per-block, generic and warp-per-block-pair kernels are checked
+    against the oracle independently."""
+    old = pkg.dct16a_get_option(pkg.OPT_CODEC_PATH)
+    pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, request.param)
+    yield request.param
+    pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, old)
+
+
 def _codec_check(imgs, mode, bit_depth, r=16, step=16, valid_height=None):
     x = to_dev(imgs)
     rec, sse, ps = pkg.codec(x, mode, r=r, step=step, valid_height=valid_height)
@@ -190,37 +201,37 @@ def _codec_check(imgs, mode, bit_depth, r=16, step=16, valid_height=None):
     return rec
 
 
-def test_codec_config1():
+def test_codec_config1(codec_path):
     _codec_check(synth.image_u8(0)[None], "zonal", 8, r=16)
 
 
 @pytest.mark.parametrize("r", [1, 2, 10, 11, 16, 21, 22, 32, 36, 37, 100, 256])
-def test_codec_zonal_varied(r):
+def test_codec_zonal_varied(r, codec_path):
     # r <= 36 runs the thread-per-block kernel (bands 3/5/7), larger r the generic one
     imgs = np.concatenate([synth.batch_u8([40, 41], 48, 272), synth.adversarial_u8(48, 272)])
     _codec_check(imgs, "zonal", 8, r=r)
 
 
 @pytest.mark.parametrize("shape", [(1, 16, 16), (3, 32, 48), (2, 64, 1920), (1, 48, 784)])
-def test_codec_zonal_shapes(shape):
+def test_codec_zonal_shapes(shape, codec_path):
     n, h, w = shape
     imgs = synth.batch_u8(range(60, 60 + n), h, w)
     for r in (16, 32):
         _codec_check(imgs, "zonal", 8, r=r)
 
 
-def test_codec_zonal_padded_valid_height():
+def test_codec_zonal_padded_valid_height(codec_path):
     v = synth.video_u8(3, H=56, W=96, pad_to=64, workers=1)
     _codec_check(v, "zonal", 8, r=32, valid_height=56)
 
 
-def test_codec_uniform():
+def test_codec_uniform(codec_path):
     f = np.concatenate([synth.frames_10bit([6, 7], H=64, W=128, workers=1),
                         synth.adversarial_u8(64, 128, bit_depth=10)])
     _codec_check(f, "uniform", 10, step=16)
 
 
-def test_codec_equals_chain():
+def test_codec_equals_chain(codec_path):
     imgs = synth.batch_u8([50, 51], 64, 64)
     for mode, r, step, bd, src in [("zonal", 16, 16, 8, imgs),
                                    ("uniform", 16, 16, 10, synth.frames_10bit([8], H=64, W=64, workers=1))]:
@@ -230,12 +241,76 @@ def test_codec_equals_chain():
         assert np.array_equal(rec.cpu().numpy(), rec_chain)
 
 
-def test_codec_without_recon_output():
+def test_codec_without_recon_output(codec_path):
     img = synth.image_u8(1)[None]
     x = to_dev(img)
     _, sse, ps = pkg.codec(x, "zonal", r=16, want_recon=False)
     torch.cuda.synchronize()
     assert sse.cpu().tolist() == oc.codec_images(img, "zonal", r=16)["sse"]
+    f = synth.frames_10bit([12], H=48, W=208, workers=1)
+    _, sse, ps = pkg.codec(to_dev(f), "uniform", step=16, want_recon=False)
+    torch.cuda.synchronize()
+    assert sse.cpu().tolist() == oc.codec_images(f, "uniform", step=16, bit_depth=10)["sse"]
+
+
+@pytest.mark.parametrize("step", [1, 3, 16, 24, 200, 65535])
+@pytest.mark.parametrize("shape", [(1, 16, 16), (2, 48, 208), (1, 32, 1920)])
+def test_codec_uniform_steps_and_shapes(step, shape, codec_path):
+    """Uniform codec (warp kernel) for small to huge steps, a single block, a
+    ragged tile (13 blocks per strip) and a wide strip, 10-bit and 8-bit."""
+    n, h, w = shape
+    f = synth.frames_10bit(list(range(20, 20 + n)), H=h, W=w, workers=1)
+    _codec_check(f, "uniform", 10, step=step)
+    u8 = synth.batch_u8(range(30, 30 + n), h, w)
+    _codec_check(u8, "uniform", 8, step=step)
+
+
+@pytest.mark.parametrize("r", [1, 16, 37, 100, 256])
+def test_codec_zonal_10bit(r, codec_path):
+    f = np.concatenate([synth.frames_10bit([14, 15], H=48, W=208, workers=1),
+                        synth.adversarial_u8(48, 208, bit_depth=10)])
+    _codec_check(f, "zonal", 10, r=r)
+
+
+def _tie_levels():
+    """Levels with exact .5 ties of the reconstruction (irrational parts
+    cancelled: only rational cells g_k = g_l populated) and near-ties, with
+    the steps that produce them (oracle pins: test_uniform_recon_exact_ties_*)."""
+    T = np.array(oc.T)
+    g = np.diag(T @ T.T)
+    rational = np.array([[g[k] == g[l] for l in range(16)] for k in range(16)])
+    rng = np.random.default_rng(17)
+    cases = []
+    q = np.zeros((4, 16, 16), dtype=np.int32)
+    q[0, 0, 0] = 1                                  # Δ=24: 1.5 everywhere
+    q[1, 0, 0], q[1, 2, 2] = 8, 1                   # Δ=6: 3 ± 1/2
+    q[2] = rng.integers(-3, 4, size=(16, 16)) * rational
+    q[2, 0, 0] = 40
+    q[3] = rng.integers(-2, 3, size=(16, 16))
+    q[3, 0, 0] = 60
+    for step in (24, 6, 12, 16):
+        cases.append((step, q.copy()))
+    r = rng.integers(-3, 4, size=(64, 16, 16)).astype(np.int32) * rational
+    r[:, 0, 0] = rng.integers(20, 90, size=64)
+    cases.append((6, r))
+    return cases
+
+
+@pytest.mark.parametrize("case", range(5))
+def test_uniform_inverse_exact_ties(case):
+    """dct16a_inverse (uniform) on levels whose reconstruction has exact .5
+    ties or near-ties: pixels must equal the oracle's exact decisions."""
+    step, q = _tie_levels()[case]
+    nb = q.shape[0]
+    want = oc.uniform_inverse_levels(q.astype(np.int64), step, bit_depth=10)
+    if step in (24, 6):
+        assert want["n_near_ties"] > 0
+    qd = to_dev(q.reshape(nb, 16, 16))
+    rec = torch.zeros((1, 16, 16 * nb), dtype=torch.int16, device=DEV)
+    pkg.dct16a_inverse(qd, rec, pkg.make_quant("uniform", step=step), pkg.desc_of(rec, 10))
+    torch.cuda.synchronize()
+    got = rec.cpu().numpy()[0].reshape(16, nb, 16).transpose(1, 0, 2)
+    assert np.array_equal(got, want["recon"])
 
 
 # ------------------------------------------------- full-size configurations
@@ -263,3 +338,45 @@ def test_config2_full_size_sampled():
         xb = x.view(n, 32, 16, 32, 16).permute(0, 1, 3, 2, 4).reshape(-1, 16, 16)[s:s + (1 << 20)].to(torch.int64)
         assert torch.equal(z[:, 0, 0], xb.sum(dim=(1, 2)))
         assert torch.equal((W * z * z).sum(dim=(1, 2)), 2304 * (xb * xb).sum(dim=(1, 2)))
+
+
+@pytest.mark.slow
+def test_config4_full_size_tiled():
+    """Config 4 geometry at full size — 1000 frames of 3840x2160 int16 (16.6 GB,
+    so every offset past frame 258 needs 64 bits) — through dct16a_codec in the
+    launch configuration tools/bench_configs.py times.  The frames repeat 8
+    distinct generated frames; every per-frame SSE and the recon of sampled
+    frames (first, middle, last) are checked against the oracle."""
+    k = 8
+    src = synth.frames_10bit(range(k))
+    sd = to_dev(src)
+    n = 1000
+    x = torch.empty((n, 2160, 3840), dtype=torch.int16, device=DEV)
+    for f in range(n):
+        x[f].copy_(sd[f % k])
+    rec, sse, ps = pkg.codec(x, "uniform", step=16)
+    torch.cuda.synchronize()
+    refs = [oc.codec_images(src[i:i + 1], "uniform", step=16, bit_depth=10) for i in range(k)]
+    got_sse = sse.cpu().tolist()
+    assert got_sse == [refs[f % k]["sse"][0] for f in range(n)]
+    for f in (0, 1, 517, n - 1):
+        assert np.array_equal(rec[f].cpu().numpy(), refs[f % k]["recon_img"][0]), f
+    for f in (0, n - 1):
+        assert abs(float(ps[f]) - refs[f % k]["psnr"][0]) < 1e-3
+
+
+@pytest.mark.slow
+def test_config3_full_size_sampled():
+    """Config 3 at full size (600 x 1920x1088 padded video, zonal r = 32,
+    PSNR over the 1080 visible rows) in the bench launch configuration;
+    sampled frames checked against the oracle."""
+    v = synth.video_u8(600)
+    x = to_dev(v)
+    rec, sse, ps = pkg.codec(x, "zonal", r=32, valid_height=1080)
+    torch.cuda.synchronize()
+    got_sse = sse.cpu().tolist()
+    for f in (0, 1, 299, 598, 599):
+        ref = oc.codec_images(v[f:f + 1], "zonal", r=32, valid_height=1080)
+        assert np.array_equal(rec[f].cpu().numpy(), ref["recon_img"][0]), f
+        assert got_sse[f] == ref["sse"][0]
+        assert abs(float(ps[f]) - ref["psnr"][0]) < 1e-3
