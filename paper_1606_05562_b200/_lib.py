@@ -11,7 +11,8 @@ import ctypes
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libdct16a.so")
+# DCT16A_LIB overrides the library path (kernel-variant experiments under tools/)
+LIB_PATH = os.environ.get("DCT16A_LIB") or os.path.join(PKG, "libdct16a.so")
 
 ZONAL = 0
 UNIFORM = 1

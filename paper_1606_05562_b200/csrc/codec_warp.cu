@@ -43,8 +43,14 @@
 namespace dct16a {
 namespace {
 
-constexpr int kWWarps = 4;    // warps per CTA
-constexpr int kWStages = 3;   // TMA ring depth per warp
+#ifndef DCT16A_CW_STAGES
+#define DCT16A_CW_STAGES 3
+#endif
+#ifndef DCT16A_CW_UCTAS
+#define DCT16A_CW_UCTAS 3
+#endif
+constexpr int kWWarps = 4;                  // warps per CTA
+constexpr int kWStages = DCT16A_CW_STAGES;  // TMA ring depth per warp
 constexpr int kWTile = 8;     // blocks per tile (128 px)
 // per-warp transposition bytes (2 blocks x 16 x 17 doubles = 4352), rounded so
 // that every warp's stages stay 1024-byte aligned (the 128-byte swizzle pattern
@@ -59,7 +65,7 @@ struct WCfg {
     static constexpr int kSmem = 1024 + kWWarps * kWarpBytes + kWWarps * kWStages * 8;
     static constexpr int kFit = (227 * 1024) / (kSmem + 1024);
     // the float64 path needs ~170 registers: at most 3 CTAs (12 warps) per SM
-    static constexpr int kCtasPerSm = UNIFORM ? (kFit < 3 ? kFit : 3) : (kFit < 4 ? kFit : 4);
+    static constexpr int kCtasPerSm = UNIFORM ? (kFit < DCT16A_CW_UCTAS ? kFit : DCT16A_CW_UCTAS) : (kFit < 4 ? kFit : 4);
 };
 
 struct WParams {
@@ -69,7 +75,7 @@ struct WParams {
     // zonal
     int r;
     // uniform
-    int step, F, wbits, hi_shift, hi_c;
+    int step, F, wbits, hi_shift, hi_c, hi_c2;
     float magic_f, half_delta;
     uint32_t magic_bits;
 };
@@ -169,6 +175,25 @@ __device__ __noinline__ void exact_levels_from_stage(const uint8_t* stage, int b
     }
 }
 
+// Rare branch of the uniform rounding: row t of the block has a pixel within
+// 2^-20 of a .5 boundary.  Recompute the row from the transposition tile (still
+// intact), flag the near pixels again and decide them exactly from the levels.
+template <int ELEM>
+__device__ __noinline__ void exact_row_fix(const uint8_t* stage, int bb, const double* urow, int t, int step,
+                                           int maxpix, int* pix) {
+    double rr[16], a[16];
+    for (int j = 0; j < 16; ++j) rr[j] = urow[j];
+    net_inv(rr, a);
+    int32_t qb[256];
+    exact_levels_from_stage<ELEM>(stage, bb, step, qb);
+    for (int j = 0; j < 16; ++j) {
+        bool nr;
+        int n0;
+        round_f64(a[j], nr, n0);
+        if (nr) pix[j] = min(max(uniform_exact_floor(qb, t, j, step, n0), 0), maxpix);
+    }
+}
+
 // Exact uniform level for a coefficient whose float estimate m is flagged (rare).
 __device__ __noinline__ int32_t uniform_fix_call(float z, int32_t m, int step, int G) {
     const uint32_t az = static_cast<uint32_t>(fabsf(z));
@@ -212,8 +237,8 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
     const int cl = uclass(l);
     float cq[3];          // uniform: 1/(Δ·sqrt(g_k·g_l)) per class of k
     double wq[3], kq[3];  // uniform: Δ·s_k·s_l and −fl(1.5·2^E·Δ·s_k·s_l)
+    uint32_t orm[3];      // uniform: all ones where the cell (k, l) is rational (never re-checked)
     float wz[16];         // zonal: W ⊙ M_r
-    uint32_t irr = 0;     // uniform: k whose cell (k, l) is irrational
     if constexpr (UNIFORM) {
         const double sl = s_of(l);
         const double Kmag = static_cast<double>(3LL << (19 - p.hi_shift));   // 1.5·2^E, E = 20 - hi_shift
@@ -224,13 +249,13 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
             cq[c] = static_cast<float>(s / p.step);
             wq[c] = static_cast<double>(p.step) * s;
             kq[c] = -(Kmag * wq[c]);
+            orm[c] = c == cl ? 0xFFFFFFFFu : 0u;
         }
-#pragma unroll
-        for (int k = 0; k < 16; ++k) irr |= (uclass(k) != cl ? 1u : 0u) << k;
     } else {
 #pragma unroll
         for (int k = 0; k < 16; ++k) wz[k] = zigzag_rank(k, l) < p.r ? static_cast<float>(w_of(k, l)) : 0.0f;
     }
+    const uint32_t fmask = (1u << p.F) - 1u;
 
     // per-warp transposition tiles: Y (float, row pitch 20, second block shifted 16 banks)
     // and U (V = double/float, row pitch 17)
@@ -288,29 +313,37 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
             {
                 V c[16], u[16];
                 if constexpr (UNIFORM) {
-                    int32_t m[16];
-                    uint32_t nm = 0;
+                    // level m = floor(e), e = |Z|·c + 1/2 + δ, from the bits of one
+                    // round-down add onto 1.5·2^(23-F): bits >> F = (magic >> F) + m and the
+                    // low F bits are the fraction.  The high word of the double 1.5·2^E + m
+                    // is one IMAD of bits >> F; the sign of Z flips the DFMA result.
+                    uint32_t nmin = 0xFFFFFFFFu;
 #pragma unroll
                     for (int k = 0; k < 16; ++k) {
-                        const float e = fmaf(fabsf(z[k]), cq[uclass(k)], p.half_delta);
-                        const uint32_t v = __float_as_uint(__fadd_rd(e, p.magic_f)) - p.magic_bits;
-                        m[k] = static_cast<int32_t>(v >> p.F);
-                        nm |= ((v & ((1u << p.F) - 1u)) < static_cast<uint32_t>(p.wbits) ? 1u : 0u) << k;
-                    }
-                    nm &= irr;
-                    if (__any_sync(0xffffffffu, nm)) {
-#pragma unroll
-                        for (int k = 0; k < 16; ++k)
-                            if ((nm >> k) & 1u) m[k] = uniform_fix_call(z[k], m[k], p.step, g_of(k) * g_of(l));
-                    }
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        const uint32_t sg = __float_as_uint(z[k]) & 0x80000000u;
-                        const double d = __hiloint2double((m[k] << p.hi_shift) + p.hi_c, 0);
                         const int ck = uclass(k);
-                        const double ws = __hiloint2double(__double2hiint(wq[ck]) ^ static_cast<int>(sg), __double2loint(wq[ck]));
-                        const double ks = __hiloint2double(__double2hiint(kq[ck]) ^ static_cast<int>(sg), __double2loint(kq[ck]));
-                        c[k] = fma(d, ws, ks);
+                        const float e = fmaf(fabsf(z[k]), cq[ck], p.half_delta);
+                        const uint32_t bits = __float_as_uint(__fadd_rd(e, p.magic_f));
+                        nmin = min(nmin, (bits & fmask) | orm[ck]);
+                        const double d = __hiloint2double(static_cast<int>((bits >> p.F) * (1u << p.hi_shift) + p.hi_c2), 0);
+                        const double cm = fma(d, wq[ck], kq[ck]);
+                        c[k] = __hiloint2double(__double2hiint(cm) ^ static_cast<int>(__float_as_uint(z[k]) & 0x80000000u),
+                                                __double2loint(cm));
+                    }
+                    // irrational cell with its fraction in the window [0, δ + 2·err): decide exactly
+                    if (__any_sync(0xffffffffu, nmin < static_cast<uint32_t>(p.wbits))) {
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) {
+                            const int ck = uclass(k);
+                            const float e = fmaf(fabsf(z[k]), cq[ck], p.half_delta);
+                            const uint32_t bits = __float_as_uint(__fadd_rd(e, p.magic_f));
+                            if (((bits & fmask) | orm[ck]) < static_cast<uint32_t>(p.wbits)) {
+                                const int32_t m = uniform_fix_call(z[k], static_cast<int32_t>((bits - p.magic_bits) >> p.F),
+                                                                   p.step, g_of(k) * g_of(l));
+                                const double d = __hiloint2double((m << p.hi_shift) + p.hi_c, 0);
+                                const double cm = fma(d, wq[ck], kq[ck]);
+                                c[k] = z[k] < 0.0f ? -cm : cm;
+                            }
+                        }
                     }
                 } else {
 #pragma unroll
@@ -330,24 +363,24 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
                 for (int j = 0; j < 16; ++j) rr[j] = tu[t * 17 + j];
                 net_inv(rr, a);
                 if constexpr (UNIFORM) {
-                    uint32_t nm = 0;
-                    int n0[16];
+                    // floor(A′ + 1/2) from one round-down add (round_f64); any pixel within
+                    // 2^-20 of a .5 boundary sends the warp to the exact decision
+                    uint32_t nmin = 0xFFFFFFFFu;
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
-                        bool nr;
-                        pix[j] = round_f64(a[j], nr, n0[j]);
-                        nm |= (nr ? 1u : 0u) << j;
+                        const double d = __dadd_rd(a[j], 1572864.5);
+                        nmin = min(nmin, static_cast<uint32_t>(__double2loint(d)) + 4096u);
+                        pix[j] = __vimin_s32_relu(__double2hiint(d) - 0x41380000, p.maxpix);
                     }
-                    if (!valid) nm = 0;
-                    if (__any_sync(0xffffffffu, nm)) {
-                        int32_t qb[256];
-                        if (nm) exact_levels_from_stage<ELEM>(stage, bb, p.step, qb);
+                    if (!valid) nmin = 0xFFFFFFFFu;
+                    if (__any_sync(0xffffffffu, nmin < 8192u) && nmin < 8192u) {
+                        int fix[16];   // local memory, rare branch only
 #pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if ((nm >> j) & 1u) pix[j] = uniform_exact_floor(qb, t, j, p.step, n0[j]);
+                        for (int j = 0; j < 16; ++j) fix[j] = pix[j];
+                        exact_row_fix<ELEM>(stage, bb, tu + t * 17, t, p.step, p.maxpix, fix);
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) pix[j] = fix[j];
                     }
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) pix[j] = min(max(pix[j], 0), p.maxpix);
                 } else {
                     const float inv2304 = 1.0f / 2304.0f;
 #pragma unroll
@@ -462,6 +495,8 @@ int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon
         while ((1 << E) <= 2 * (static_cast<int>(e_max) + 1)) ++E;
         p.hi_shift = 20 - E;
         p.hi_c = 0x3FF00000 + ((E) << 20) + (1 << 19);   // high word of 1.5·2^E
+        // the same word from bits >> F = (magic_bits >> F) + m (arithmetic mod 2^32)
+        p.hi_c2 = static_cast<int>(static_cast<uint32_t>(p.hi_c) - ((p.magic_bits >> p.F) << p.hi_shift));
     }
     static bool attr = false;
     if (!attr) {
