@@ -144,6 +144,22 @@ DCT16A_API int dct16a_codec(const void* src, const dct16a_desc* desc,
                             uint64_t* sse, double* psnr, void* stream);
 
 /*
+ * dct16a_zonal_sweep — the zonal path of dct16a_codec for every retained
+ * count r = r_first .. r_first + r_count - 1 in one pass over the images: the
+ * r-sweep of the paper's compression experiment (Figs. 1-2;
+ * config 5).  Since M_r adds one zig-zag cell (k, l) to M_{r-1}, the exact
+ * numerator is updated by W_kl·Z_kl·T_k ⊗ T_l per step; every per-r result is
+ * identical to dct16a_codec(mode = zonal, r, recon = NULL).
+ *   sse  : uint64 out [batch][r_count]; sse[n·r_count + i] is the SSE of image
+ *          n over its valid rows reconstructed with r = r_first + i.
+ *   psnr : optional float64 out, same layout (+INFINITY where SSE = 0).
+ * Errors: DCT16A_EDOMAIN unless 1 <= r_first and r_first + r_count - 1 <= 256
+ * with r_count >= 1.  Work grows with r_first + r_count (the sweep starts at 1).
+ */
+DCT16A_API int dct16a_zonal_sweep(const void* src, const dct16a_desc* desc, int32_t r_first,
+                                  int32_t r_count, uint64_t* sse, double* psnr, void* stream);
+
+/*
  * dct16a_set_option / dct16a_get_option — process-wide knobs for tuning and
  * cross-checking; they never change results (every kernel choice computes the
  * same bytes).  Initial values come from the environment variables named

@@ -10,7 +10,7 @@ from __future__ import annotations
 
 from ._lib import (OPT_CODEC_PATH, OPT_FWD_STORE, UNIFORM, ZONAL, Dct16aError, Desc, Quant,  # noqa: F401
                    dct16a_codec, dct16a_forward, dct16a_get_option, dct16a_inverse, dct16a_last_error,
-                   dct16a_psnr, dct16a_quantize, dct16a_set_option, dct16a_version, desc_of, lib,
+                   dct16a_psnr, dct16a_quantize, dct16a_set_option, dct16a_version, dct16a_zonal_sweep, desc_of, lib,
                    make_desc, make_quant)
 
 __version__ = "0.1.0"
@@ -42,6 +42,19 @@ def codec(images, mode="zonal", r=16, step=16, valid_height=None, want_recon=Tru
     recon = torch.empty_like(images) if want_recon else None
     dct16a_codec(images, make_quant(mode, r, step), sse, recon, psnr, d, stream)
     return recon, sse, psnr
+
+
+def zonal_sweep(images, r_first=1, r_count=256, valid_height=None, stream=None):
+    """SSE and PSNR of the zonal codec for every r in [r_first, r_first + r_count)
+    in one pass (config 5).  Returns (sse int64[batch, r_count], psnr float64[batch, r_count])."""
+    import torch
+    if images.dim() == 2:
+        images = images.unsqueeze(0)
+    n = images.shape[0]
+    sse = torch.empty((n, r_count), dtype=torch.int64, device=images.device)
+    psnr = torch.empty((n, r_count), dtype=torch.float64, device=images.device)
+    dct16a_zonal_sweep(images, r_first, r_count, sse, psnr, desc_of(images, valid_height=valid_height), stream)
+    return sse, psnr
 
 
 def forward_host(host_images, host_coef, chunk_images=256, device=None, bufs=None):

@@ -217,6 +217,21 @@ DCT16A_API int dct16a_codec(const void* src, const dct16a_desc* desc, const dct1
                     "dct16a_codec");
 }
 
+DCT16A_API int dct16a_zonal_sweep(const void* src, const dct16a_desc* desc, int32_t r_first, int32_t r_count,
+                                  uint64_t* sse, double* psnr, void* stream) {
+    Geom g;
+    int rc;
+    if ((rc = check_desc(desc, &g))) return rc;
+    if ((rc = check_ptr(src, "src"))) return rc;
+    if (r_first < 1 || r_count < 1 || r_first + r_count - 1 > 256)
+        return fail(DCT16A_EDOMAIN, "r range [%d, %d] outside [1, 256]", r_first, r_first + r_count - 1);
+    if (!sse) return fail(DCT16A_ENULL, "sse is NULL");
+    if (reinterpret_cast<uintptr_t>(sse) & 7u) return fail(DCT16A_EALIGN, "sse is not 8-byte aligned");
+    if (psnr && (reinterpret_cast<uintptr_t>(psnr) & 7u)) return fail(DCT16A_EALIGN, "psnr not 8-byte aligned");
+    return launched(launch_sweep(src, g, r_first, r_count, sse, psnr, static_cast<cudaStream_t>(stream)),
+                    "dct16a_zonal_sweep");
+}
+
 DCT16A_API int dct16a_set_option(int option, int value) {
     if (option == DCT16A_OPT_CODEC_PATH) {
         if (value < 0 || value > 2) return fail(DCT16A_EDOMAIN, "codec path %d not in [0, 2]", value);

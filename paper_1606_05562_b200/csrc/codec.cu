@@ -352,14 +352,19 @@ __global__ void psnr_kernel(const unsigned long long* sse, double* psnr, int n, 
     psnr[i] = s == 0 ? INFINITY : 10.0 * log10(peak2P / static_cast<double>(s));
 }
 
-namespace {
-int finish_psnr(const Geom& g, uint64_t* sse, double* psnr, cudaStream_t st) {
+// PSNR of `count` SSE values of images of geometry g (peak 2^b - 1, P = VH·W).
+int launch_psnr_finish(const Geom& g, long long count, uint64_t* sse, double* psnr, cudaStream_t st) {
     if (!psnr) return 0;
     const double peak = static_cast<double>((1 << g.bits) - 1);
     const double P = static_cast<double>(g.VH) * g.W;
-    psnr_kernel<<<(g.N + 127) / 128, 128, 0, st>>>(reinterpret_cast<unsigned long long*>(sse), psnr, g.N,
-                                                  peak * peak * P);
+    psnr_kernel<<<static_cast<unsigned>((count + 127) / 128), 128, 0, st>>>(reinterpret_cast<unsigned long long*>(sse),
+                                                                         psnr, static_cast<int>(count), peak * peak * P);
     return static_cast<int>(cudaGetLastError());
+}
+
+namespace {
+int finish_psnr(const Geom& g, uint64_t* sse, double* psnr, cudaStream_t st) {
+    return launch_psnr_finish(g, g.N, sse, psnr, st);
 }
 }  // namespace
 

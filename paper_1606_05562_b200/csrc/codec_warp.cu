@@ -38,6 +38,7 @@
 #include "ptx.cuh"
 #include "quant.cuh"
 #include "tables.cuh"
+#include "tile128.cuh"
 #include "uexact.cuh"
 
 namespace dct16a {
@@ -51,7 +52,6 @@ namespace {
 #endif
 constexpr int kWWarps = 4;                  // warps per CTA
 constexpr int kWStages = DCT16A_CW_STAGES;  // TMA ring depth per warp
-constexpr int kWTile = 8;     // blocks per tile (128 px)
 // per-warp transposition bytes (2 blocks x 16 x 17 doubles = 4352), rounded so
 // that every warp's stages stay 1024-byte aligned (the 128-byte swizzle pattern
 // is taken from smem address bits 7-9)
@@ -79,72 +79,6 @@ struct WParams {
     float magic_f, half_delta;
     uint32_t magic_bits;
 };
-
-__device__ __forceinline__ uint8_t* walign1024(uint8_t* smem_raw) {
-    return smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
-}
-
-// byte offset of the 16-byte chunk c of row t in a 128-byte-swizzled box
-__device__ __forceinline__ int swz(int t, int c) { return t * 128 + ((c ^ (t & 7)) << 4); }
-
-template <int ELEM>
-__device__ __forceinline__ void w_tile_coords(const WParams& p, long long tix, int* n, int* by, int* x0) {
-    const long long strip = tix / p.tiles_per_strip;
-    const int tb = static_cast<int>(tix - strip * p.tiles_per_strip);
-    *n = static_cast<int>(strip / p.BY);
-    *by = static_cast<int>(strip - static_cast<long long>(*n) * p.BY);
-    *x0 = tb * kWTile * 16;
-}
-
-template <int ELEM>
-__device__ __forceinline__ void w_issue(const CUtensorMap* tin, const WParams& p, long long tix, uint8_t* stage,
-                                        uint64_t* bar, uint64_t pol) {
-    int n, by, x0;
-    w_tile_coords<ELEM>(p, tix, &n, &by, &x0);
-    constexpr int box_px = 128 / ELEM;
-    const int nbox = (ELEM == 2 && x0 + box_px < p.W) ? 2 : 1;
-    mbar_arrive_expect_tx(bar, static_cast<uint32_t>(nbox * 2048));
-    for (int h = 0; h < nbox; ++h) tma_load_3d(stage + h * 2048, tin, bar, x0 + h * box_px, by * 16, n, pol);
-}
-
-template <int ELEM>
-__device__ __forceinline__ void w_store(const CUtensorMap* tout, const WParams& p, long long tix, uint8_t* stage) {
-    int n, by, x0;
-    w_tile_coords<ELEM>(p, tix, &n, &by, &x0);
-    constexpr int box_px = 128 / ELEM;
-    const int nbox = (ELEM == 2 && x0 + box_px < p.W) ? 2 : 1;
-    for (int h = 0; h < nbox; ++h) tma_store_3d(tout, stage + h * 2048, x0 + h * box_px, by * 16, n);
-}
-
-// smem byte offsets (within the stage) of the 16·ELEM bytes of row t of block bb
-template <int ELEM>
-__device__ __forceinline__ void row_addr(int bb, int t, int* a0, int* a1) {
-    if (ELEM == 1) {
-        *a0 = swz(t, bb);
-        *a1 = *a0;
-    } else {
-        const int base = (bb >> 2) * 2048, c = (bb & 3) * 2;
-        *a0 = base + swz(t, c);
-        *a1 = base + swz(t, c + 1);
-    }
-}
-
-template <int ELEM>
-__device__ __forceinline__ void load_px(const uint8_t* stage, int a0, int a1, uint32_t (&w)[4 * ELEM]) {
-    const uint4 v = *reinterpret_cast<const uint4*>(stage + a0);
-    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
-    if (ELEM == 2) {
-        const uint4 u = *reinterpret_cast<const uint4*>(stage + a1);
-        w[4] = u.x; w[5] = u.y; w[6] = u.z; w[7] = u.w;
-    }
-}
-
-// pixel j of a packed row (u8 or u16)
-template <int ELEM>
-__device__ __forceinline__ int px_of(const uint32_t (&w)[4 * ELEM], int j) {
-    return ELEM == 1 ? static_cast<int>((w[j >> 2] >> (8 * (j & 3))) & 0xFFu)
-                     : static_cast<int>((w[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
-}
 
 // Exact levels of one block recomputed from its pixels (rare branch): Z by the
 // integer network, then the exact uniform decision (uniform_level/uniform_fix).

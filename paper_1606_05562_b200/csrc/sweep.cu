@@ -1,0 +1,268 @@
+// sweep.cu — the zonal codec for a whole range of retained-coefficient counts
+// r in one pass over the images (config 5: the r-sweep of the paper's image
+// compression experiment, Figs. 1-2; reading A4 zig-zag).
+//
+// With S folded into the weights the exact reconstruction
+// numerator of dct16a_codec is N_r = Tᵀ·(W ⊙ M_r ⊙ Z)·T, and M_r differs from
+// M_{r-1} in the single zig-zag cell (k, l) of rank r-1, so
+//     N_r = N_{r-1} + W_kl·Z_kl · T_k ⊗ T_l        (outer product of rows of T).
+// Every step is a rank-1 update of the 16x16 numerator followed by the same
+// rounding (reading A6) and SSE as the fused codec; the pixels for every r are
+// therefore byte-identical to dct16a_codec with that r.
+//
+// Layout: one warp holds a block pair, lane = row i of its block (as in
+// codec_warp.cu): TMA tile ring in the 128-byte swizzle (tile128.cuh), row
+// pass, smem transposition, column pass (lane = column l) producing W ⊙ Z into
+// smem, then the sweep with lane = row i: N[i][:] += (W·Z_kl·T_ki)·T_l[:] in
+// float32 (exact: half-integers below 2^23, the +1152.5 rounding offset rides
+// in N from the start), pixel = floor(N/2304) by one round-down FMA, clamp,
+// squared error in float32 (exact below 2^24 per row), one REDUX per r and a
+// shared-memory 64-bit atomic into the warp's per-r SSE, flushed to global per
+// image.
+#include <cuda.h>
+#include <stdint.h>
+
+#include "internal.h"
+#include "net16.cuh"
+#include "ptx.cuh"
+#include "tables.cuh"
+#include "tile128.cuh"
+
+namespace dct16a {
+namespace {
+
+constexpr int kSWarps = 4;    // warps per CTA
+constexpr int kSStages = 3;   // TMA ring depth per warp
+
+// zig-zag order as a table: kZZ[r] = 16·k + l of the cell with rank r (reading A4)
+struct ZZTable {
+    uint8_t v[256];
+};
+constexpr ZZTable make_zz() {
+    ZZTable t{};
+    for (int k = 0; k < 16; ++k)
+        for (int l = 0; l < 16; ++l) t.v[zigzag_rank(k, l)] = static_cast<uint8_t>(16 * k + l);
+    return t;
+}
+__constant__ ZZTable c_zz = make_zz();
+
+template <int ELEM>
+struct SCfg {
+    static constexpr int kStageBytes = 16 * kWTile * 16 * ELEM;
+    // per warp: stages | Y transposition (2 x 336 floats) | W⊙Z (2 x 256 floats) | SSE[256] u64
+    static constexpr int kYBytes = 3072, kZBytes = 2048, kSseBytes = 2048;
+    static constexpr int kWarpBytes = kSStages * kStageBytes + kYBytes + kZBytes + kSseBytes;
+    static_assert(kWarpBytes % 1024 == 0, "stages must stay 1024-byte aligned");
+    static constexpr int kTBytes = 1024;   // T as floats, shared by the CTA
+    static constexpr int kSmem = 1024 + kSWarps * kWarpBytes + kTBytes + kSWarps * kSStages * 8;
+    static constexpr int kFit = (227 * 1024) / (kSmem + 1024);
+    static constexpr int kCtasPerSm = kFit < 4 ? kFit : 4;
+};
+
+struct SParams {
+    int W, BX, BY, VH, tiles_per_strip, maxpix;
+    long long n_tiles, chunk;
+    int r_first, r_count, r_last;
+};
+
+}  // namespace
+
+template <int ELEM>
+__global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
+    sweep_kernel(const __grid_constant__ CUtensorMap tin, unsigned long long* __restrict__ sse, const SParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = walign1024(smem_raw);
+    using Cfg = SCfg<ELEM>;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int h = lane >> 4, t = lane & 15;
+    uint8_t* wbase = smem + warp * Cfg::kWarpBytes;
+    float* ty = reinterpret_cast<float*>(wbase + kSStages * Cfg::kStageBytes) + h * (16 * 20 + 16);
+    float* wzb = reinterpret_cast<float*>(wbase + kSStages * Cfg::kStageBytes + Cfg::kYBytes);
+    float* wz = wzb + h * 256;
+    unsigned long long* ssew =
+        reinterpret_cast<unsigned long long*>(wbase + kSStages * Cfg::kStageBytes + Cfg::kYBytes + Cfg::kZBytes);
+    float* Ts = reinterpret_cast<float*>(smem + kSWarps * Cfg::kWarpBytes);   // Ts[k*16 + i] = T[k][i]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSWarps * Cfg::kWarpBytes + Cfg::kTBytes) + warp * kSStages;
+
+    // T from the network of Eq. (1): column i = net_fwd(e_i)
+    if (threadIdx.x < 16) {
+        float x[16], y[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x[j] = j == static_cast<int>(threadIdx.x) ? 1.0f : 0.0f;
+        net_fwd(x, y);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) Ts[k * 16 + threadIdx.x] = y[k];
+    }
+    for (int i = lane; i < 256; i += 32) ssew[i] = 0;
+
+    const long long gw = static_cast<long long>(blockIdx.x) * kSWarps + warp;
+    const long long t0 = gw * p.chunk;
+    long long t1 = t0 + p.chunk;
+    if (t1 > p.n_tiles) t1 = p.n_tiles;
+    const uint64_t pol = policy_evict_first();
+    if (lane == 0) {
+        for (int s = 0; s < kSStages; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+        prefetch_tmap(&tin);
+        for (int s = 0; s < kSStages - 1; ++s)
+            if (t0 + s < t1) w_issue<ELEM>(&tin, p, t0 + s, wbase + s * Cfg::kStageBytes, &bars[s], pol);
+    }
+    __syncthreads();
+
+    // per-lane weights of column l = t by class of k: W = 2304/(g_k·g_l)
+    const int l = t;
+    const float w16 = static_cast<float>(2304 / (16 * g_of(l)));
+    const float w12 = static_cast<float>(2304 / (12 * g_of(l)));
+    const float w8 = static_cast<float>(2304 / (8 * g_of(l)));
+    const float inv2304 = 1.0f / 2304.0f;
+    const float top = 8388608.0f + static_cast<float>(p.maxpix);
+
+    int cur_n = -1;
+    int it = 0;
+    for (long long tix = t0; tix < t1; ++tix, ++it) {
+        const int s = it % kSStages;
+        uint8_t* stage = wbase + s * Cfg::kStageBytes;
+        mbar_wait(&bars[s], (it / kSStages) & 1);
+        int n, by, x0;
+        w_tile_coords<ELEM>(p, tix, &n, &by, &x0);
+        if (n != cur_n) {   // flush the per-r SSE of the previous image (warp-uniform)
+            __syncwarp();
+            if (cur_n >= 0)
+                for (int i = lane; i < p.r_count; i += 32) {
+                    if (ssew[i]) atomicAdd(sse + static_cast<long long>(cur_n) * p.r_count + i, ssew[i]);
+                    ssew[i] = 0;
+                }
+            __syncwarp();
+            cur_n = n;
+        }
+        const int nb = min(kWTile, p.BX - x0 / 16);
+        const bool row_valid = by * 16 + t < p.VH;
+#pragma unroll 1
+        for (int pair = 0; 2 * pair < nb; ++pair) {
+            const int bb = 2 * pair + h;
+            const bool contributes = bb < nb && row_valid;
+            int a0, a1;
+            row_addr<ELEM>(bb, t, &a0, &a1);
+            float xs[16];   // 2^23 + x[i][j], the SSE reference in the magic-float domain
+            {
+                uint32_t w[4 * ELEM];
+                load_px<ELEM>(stage, a0, a1, w);
+                float x[16], y[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    x[j] = static_cast<float>(px_of<ELEM>(w, j));
+                    xs[j] = 8388608.0f + x[j];
+                }
+                net_fwd(x, y);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    *reinterpret_cast<float4*>(ty + t * 20 + 4 * q) = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+            }
+            __syncwarp();
+            {
+                float col[16], z[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) col[k] = ty[k * 20 + l];
+                net_fwd(col, z);
+#pragma unroll
+                for (int k = 0; k < 16; ++k)
+                    wz[k * 16 + l] = z[k] * (g_of(k) == 16 ? w16 : (g_of(k) == 12 ? w12 : w8));
+            }
+            __syncwarp();
+            // ---- the sweep, lane = row i = t
+            float N[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) N[j] = 1152.5f;
+#pragma unroll 1
+            for (int r = 1; r <= p.r_last; ++r) {
+                const int kl = c_zz.v[r - 1];
+                const int k = kl >> 4, lc = kl & 15;
+                const float sv = wz[kl] * Ts[k * 16 + t];
+                const float4* tr = reinterpret_cast<const float4*>(Ts + lc * 16);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float4 tq = tr[q];
+                    N[4 * q] = fmaf(sv, tq.x, N[4 * q]);
+                    N[4 * q + 1] = fmaf(sv, tq.y, N[4 * q + 1]);
+                    N[4 * q + 2] = fmaf(sv, tq.z, N[4 * q + 2]);
+                    N[4 * q + 3] = fmaf(sv, tq.w, N[4 * q + 3]);
+                }
+                if (r >= p.r_first) {
+                    float e = 0.0f;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        // floor((N + 1152.5)/2304) + 2^23 by one round-down FMA (exact, see header)
+                        const float f = fminf(fmaxf(__fmaf_rd(N[j], inv2304, 8388608.0f), 8388608.0f), top);
+                        const float d = f - xs[j];
+                        e = fmaf(d, d, e);
+                    }
+                    const unsigned tot = __reduce_add_sync(0xffffffffu, contributes ? __float2uint_rn(e) : 0u);
+                    if (lane == 0 && tot) atomicAdd(&ssew[r - p.r_first], static_cast<unsigned long long>(tot));
+                }
+            }
+            __syncwarp();
+        }
+        if (lane == 0) {
+            const long long nt = tix + kSStages - 1;
+            if (nt < t1) w_issue<ELEM>(&tin, p, nt, wbase + ((it + kSStages - 1) % kSStages) * Cfg::kStageBytes,
+                                       &bars[(it + kSStages - 1) % kSStages], pol);
+        }
+        __syncwarp();
+    }
+    __syncwarp();
+    if (cur_n >= 0)
+        for (int i = lane; i < p.r_count; i += 32)
+            if (ssew[i]) atomicAdd(sse + static_cast<long long>(cur_n) * p.r_count + i, ssew[i]);
+}
+
+namespace {
+
+template <int ELEM>
+int launch_sweep_t(const void* src, const Geom& g, int r_first, int r_count, uint64_t* sse, cudaStream_t st) {
+    using Cfg = SCfg<ELEM>;
+    CUtensorMap tin;
+    const uint64_t dims[3] = {uint64_t(g.W), uint64_t(g.H), uint64_t(g.N)};
+    const uint64_t strides[2] = {uint64_t(g.pitch), uint64_t(g.istride)};
+    const uint32_t box[3] = {uint32_t(128 / ELEM), 16u, 1u};
+    if (encode_tiled(&tin, ELEM == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, src, dims,
+                     strides, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
+        return DCT16A_ECUDA;
+    SParams p{};
+    p.W = g.W;
+    p.BX = g.BX;
+    p.BY = g.BY;
+    p.VH = g.VH;
+    p.tiles_per_strip = (g.BX + kWTile - 1) / kWTile;
+    p.maxpix = (1 << g.bits) - 1;
+    p.n_tiles = static_cast<long long>(g.N) * g.BY * p.tiles_per_strip;
+    p.r_first = r_first;
+    p.r_count = r_count;
+    p.r_last = r_first + r_count - 1;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(sweep_kernel<ELEM>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+        attr = true;
+    }
+    long long warps = static_cast<long long>(num_sms()) * Cfg::kCtasPerSm * kSWarps;
+    if (warps > p.n_tiles) warps = p.n_tiles;
+    p.chunk = (p.n_tiles + warps - 1) / warps;
+    const long long grid = (warps + kSWarps - 1) / kSWarps;
+    sweep_kernel<ELEM><<<static_cast<unsigned>(grid), kSWarps * 32, Cfg::kSmem, st>>>(
+        tin, reinterpret_cast<unsigned long long*>(sse), p);
+    return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace
+
+int launch_sweep(const void* src, const Geom& g, int r_first, int r_count, uint64_t* sse, double* psnr,
+                 cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(uint64_t) * g.N * r_count, st);
+    if (e) return static_cast<int>(e);
+    const int rc = g.elem == 1 ? launch_sweep_t<1>(src, g, r_first, r_count, sse, st)
+                               : launch_sweep_t<2>(src, g, r_first, r_count, sse, st);
+    if (rc) return rc;
+    return launch_psnr_finish(g, static_cast<long long>(g.N) * r_count, sse, psnr, st);
+}
+
+}  // namespace dct16a

@@ -170,6 +170,11 @@ def video_u8(n: int = 600, H: int = 1080, W: int = 1920, pad_to: int = 1088, see
     return out
 
 
+def config5_images(workers: int | None = None) -> np.ndarray:
+    """Config 5: 64 images 1024x1024, seeds 100..163, rho by group of 16 (cfg5_rho)."""
+    return batch_u8(range(100, 164), 1024, 1024, rho=cfg5_rho, workers=workers)
+
+
 # ---------------------------------------------------- adversarial fixtures
 def adversarial_u8(H: int = 64, W: int = 64, bit_depth: int = 8, seed: int = 7) -> np.ndarray:
     """Edge-case images: all-0, all-max, checkerboards, impulses, stripes,

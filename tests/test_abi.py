@@ -23,7 +23,7 @@ def declared_symbols():
 def test_library_loads_and_exports_header_symbols():
     L = pkg.lib()
     syms = declared_symbols()
-    assert len(syms) == 9
+    assert len(syms) == 10
     for s in syms:
         assert hasattr(L, s), s
     out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
@@ -118,3 +118,15 @@ def test_options_validate_and_round_trip():
         pkg.dct16a_set_option(99, 0)
     assert e.value.code == -5
     assert pkg.dct16a_get_option(pkg.OPT_FWD_STORE) in range(-1, 6)
+
+
+def test_zonal_sweep_validation():
+    import torch
+    L = pkg.lib()
+    d = pkg.make_desc(64, 64, 1, 8)
+    buf = ctypes.c_void_p(1 << 20)          # aligned dummy pointers: validation fails before any use
+    for r0, rc in [(0, 5), (1, 0), (250, 8), (-3, 4)]:
+        assert L.dct16a_zonal_sweep(buf, ctypes.byref(d), r0, rc, buf, None, None) == -5
+    assert L.dct16a_zonal_sweep(buf, ctypes.byref(d), 1, 256, None, None, None) == -1
+    assert L.dct16a_zonal_sweep(buf, ctypes.byref(d), 1, 256, ctypes.c_void_p((1 << 20) + 4), None, None) == -4
+    del torch

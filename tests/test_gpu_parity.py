@@ -380,3 +380,62 @@ def test_config3_full_size_sampled():
         assert np.array_equal(rec[f].cpu().numpy(), ref["recon_img"][0]), f
         assert got_sse[f] == ref["sse"][0]
         assert abs(float(ps[f]) - ref["psnr"][0]) < 1e-3
+
+
+# ------------------------------------------------------ config 5: r-sweep
+def _sweep_check(imgs, bd, r_first, r_count, valid_height=None):
+    x = to_dev(imgs)
+    sse, ps = pkg.zonal_sweep(x, r_first, r_count, valid_height=valid_height)
+    torch.cuda.synchronize()
+    got = sse.cpu().numpy()
+    gps = ps.cpu().numpy()
+    for i, r in enumerate(range(r_first, r_first + r_count)):
+        ref = oc.codec_images(imgs, "zonal", r=r, bit_depth=bd, valid_height=valid_height)
+        assert got[:, i].tolist() == ref["sse"], r
+        for a, b in zip(gps[:, i].tolist(), ref["psnr"]):
+            assert (math.isinf(a) and math.isinf(b)) or abs(a - b) < 1e-3
+    return got
+
+
+@pytest.mark.parametrize("bd", [8, 10])
+def test_zonal_sweep_every_r(bd):
+    """dct16a_zonal_sweep: SSE and PSNR for every r = 1..256 equal the oracle's
+    zonal codec with that r (ragged tile, adversarial blocks, 8/10-bit)."""
+    if bd == 8:
+        imgs = np.concatenate([synth.batch_u8([70, 71], 48, 208), synth.adversarial_u8(48, 208)])
+    else:
+        imgs = np.concatenate([synth.frames_10bit([16], H=48, W=208, workers=1),
+                               synth.adversarial_u8(48, 208, bit_depth=10)])
+    got = _sweep_check(imgs, bd, 1, 256)
+    assert np.all(got[:, -1] == 0)                       # r = 256 is lossless
+
+
+def test_zonal_sweep_subrange_and_valid_height(codec_path):
+    v = synth.video_u8(2, H=40, W=272, pad_to=48, workers=1)
+    got = _sweep_check(v, 8, 30, 40, valid_height=40)
+    # and the same numbers from the fused codec, r by r
+    x = to_dev(v)
+    for i, r in enumerate((30, 36, 37, 69)):
+        _, sse, _ = pkg.codec(x, "zonal", r=r, valid_height=40, want_recon=False)
+        torch.cuda.synchronize()
+        assert sse.cpu().tolist() == got[:, r - 30].tolist()
+
+
+@pytest.mark.slow
+def test_config5_full_size_sampled():
+    """Config 5 at full size (64 x 1024² images, r = 1..256 in one sweep):
+    every r of one image per rho group against the oracle."""
+    imgs = synth.config5_images()
+    x = to_dev(imgs)
+    sse, ps = pkg.zonal_sweep(x, 1, 256)
+    torch.cuda.synchronize()
+    got = sse.cpu().numpy()
+    assert np.all(got[:, 255] == 0)
+    for n in (0, 16, 32, 48):
+        img = imgs[n:n + 1]
+        X = oc.to_blocks(img.astype(np.int64))
+        Z = oc.forward(X)
+        for r in range(1, 257):
+            N = oc.zonal_numerator(oc.zonal_stage(Z, r))
+            rec = oc.clamp_pixels(oc.round_half_away_rational(N, 2304), 8)
+            assert int(got[n, r - 1]) == oc.sse(img, oc.from_blocks(rec))[0], (n, r)

@@ -31,7 +31,7 @@ def timeit(fn, reps, warm=3):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="1,3,4")
+    ap.add_argument("--configs", default="1,3,4,5")
     ap.add_argument("--cfg3-frames", type=int, default=600)
     ap.add_argument("--cfg4-frames", type=int, default=1000)
     ap.add_argument("--reps", type=int, default=10)
@@ -50,6 +50,8 @@ def main():
             x = torch.from_numpy(synth.video_u8(args.cfg3_frames)).cuda()
             kw = dict(mode="zonal", r=32)
             vh = 1080
+        elif c == 5:
+            x = torch.from_numpy(synth.config5_images()).cuda()
         elif c == 4:
             n = args.cfg4_frames
             x = torch.empty((n, 2160, 3840), dtype=torch.int16, device="cuda")
@@ -61,10 +63,18 @@ def main():
         gen_s = time.time() - t0
         n, h, w = x.shape
         blocks = n * (h // 16) * (w // 16)
+        extra = {}
         if c == 2:
             coef = torch.empty((blocks, 16, 16), dtype=torch.int32, device="cuda")
             ms = timeit(lambda: pkg.dct16a_forward(x, coef, pkg.desc_of(x)), args.reps)
             alg = blocks * 1280
+        elif c == 5:
+            sse = torch.empty((n, 256), dtype=torch.int64, device="cuda")
+            ps = torch.empty((n, 256), dtype=torch.float64, device="cuda")
+            d = pkg.desc_of(x)
+            ms = timeit(lambda: pkg.dct16a_zonal_sweep(x, 1, 256, sse, ps, d), args.reps)
+            alg = blocks * 256
+            extra = {"block_evals": blocks * 256, "block_evals_per_s": blocks * 256 / ms * 1e3}
         else:
             recon = torch.empty_like(x)
             d = pkg.desc_of(x, valid_height=vh)
@@ -75,7 +85,7 @@ def main():
             alg = blocks * 2 * 256 * x.element_size()
         print(json.dumps({"config": c, "blocks": blocks, "ms": ms, "blocks_per_s": blocks / ms * 1e3,
                           "alg_GBs": alg / ms / 1e6, "frac_of_measured_hbm": alg / ms / 1e6 / peak,
-                          "gen_s": round(gen_s, 1)}), flush=True)
+                          "gen_s": round(gen_s, 1), **extra}), flush=True)
         del x
         torch.cuda.empty_cache()
 
