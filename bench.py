@@ -264,7 +264,8 @@ def run_ours(args):
                 "gpu_launches": args.steps}
         if world == 1 and not args.no_cpu_baseline:
             workers = host_cores()
-            n_s = int(os.environ.get("DCT16A_ORACLE_IMAGES", "1024"))
+            # all 4096 images: ~25 CPU-s of oracle work, ~2 s of wall time on a 16-core host
+            n_s = int(os.environ.get("DCT16A_ORACLE_IMAGES", "4096"))
             r, cpu, wall = oracle_rate(n_s, workers)
             line["cpu_baseline"] = {"value": r, "unit": "blocks/s", "cores": workers, "kind": "oracle",
                                     "sample": f"{n_s} of the 4096 config-2 images ({n_s * BLOCKS_PER_IMG} blocks), "
