@@ -45,6 +45,13 @@ __device__ __forceinline__ int32_t uniform_level(int32_t z, float c, uint64_t d2
     return z < 0 ? -m : m;
 }
 
+// cvt.pack.sat: (sat_u8(a) << 8) | sat_u8(b) | (c << 16); saturation clamps to [0, 255]
+__device__ __forceinline__ uint32_t pack2_sat_u8(int a, int b, uint32_t c) {
+    uint32_t d;
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
 __device__ __forceinline__ int zonal_pixel(int32_t N, int maxpix) {
     // round half away of N/2304, clamped to [0, maxpix] (reading A6)
     const int32_t v = N + 1152;

@@ -12,8 +12,9 @@
 // * Inverse: float32 on the FMA pipe, exact: every value is a half-integer of
 //   magnitude < 2^22 (the DC input carries +1152.5 so the output is
 //   N + 1152.5, and pixel = floor((N + 1152.5)/2304) = round_half_away(N/2304)).
-//   The multiply by 1/2304 errs by < 1.2e-7·t, far below the 0.5/2304 distance
-//   of (N + 1152.5)/2304 to any integer for every t < 1800 (larger t clamp).
+//   One round-down FMA a·fl(1/2304) + 2^23 gives the floor: the product errs by
+//   < 2^-24·t, below the 1/4608 distance of (N + 1152.5)/2304 (an odd multiple
+//   of 1/4608) to any integer for every t < 3640; cvt.pack.sat clamps to [0, 255].
 // * SSE: per 4 pixels one vabsdiff4 + one dp4a against the original bytes.
 // * Data: TMA strip-tile loads into a 3-stage per-warp ring; the reconstruction
 //   overwrites the tile in place and leaves by TMA tensor store.
@@ -23,6 +24,7 @@
 #include "internal.h"
 #include "net16.cuh"
 #include "ptx.cuh"
+#include "quant.cuh"
 #include "tables.cuh"
 
 namespace dct16a {
@@ -186,9 +188,12 @@ __global__ void __launch_bounds__(kZWarps * 32, 2)
         // ---- inverse, pass 2 down every column j, pixels, SSE, in-place recon
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
+            // columns 4q+2, 4q+3 first (packed into the high half), then 4q, 4q+1
             uint32_t wrow[16];
+            int pv[16];
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
+            for (int o = 0; o < 4; ++o) {
+                const int jj = (o + 2) & 3;
                 const int j = 4 * q + jj;
                 float in[16], a[16];
 #pragma unroll
@@ -196,10 +201,12 @@ __global__ void __launch_bounds__(kZWarps * 32, 2)
                 net_inv(in, a);
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                    const float tt = fmaxf(a[i] * inv2304, 0.0f);
-                    uint32_t bits = __float_as_uint(__fadd_rd(tt, 8388608.0f));   // 0x4B000000 + floor(tt)
-                    bits = min(bits, 0x4B0000FFu);                                // clamp 255
-                    wrow[i] = jj == 0 ? bits : __byte_perm(wrow[i], bits, jj == 1 ? 0x3240 : (jj == 2 ? 0x3410 : 0x4210));
+                    // floor((N + 1152.5)/2304) by one round-down FMA onto 2^23 (exact, header);
+                    // negative values and values above 255 saturate in the pack
+                    const int v = static_cast<int>(__float_as_uint(__fmaf_rd(a[i], inv2304, 8388608.0f)) - 0x4B000000u);
+                    if (o == 0 || o == 2) pv[i] = v;
+                    else if (o == 1) wrow[i] = pack2_sat_u8(v, pv[i], 0u);          // bytes 2, 3 (in the low half)
+                    else wrow[i] = pack2_sat_u8(v, pv[i], wrow[i]);                 // bytes 0, 1 + high half
                 }
             }
             // wrow[i] = pixels (i, 4q..4q+3); compare with the original bytes, then overwrite them
