@@ -4,6 +4,7 @@ reconstructed pixels and SSE bit-exact; float32 scaled stages within 1e-5
 relative (and exactly 0 where the oracle is 0); PSNR within 1e-3 dB.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -439,3 +440,24 @@ def test_config5_full_size_sampled():
             N = oc.zonal_numerator(oc.zonal_stage(Z, r))
             rec = oc.clamp_pixels(oc.round_half_away_rational(N, 2304), 8)
             assert int(got[n, r - 1]) == oc.sse(img, oc.from_blocks(rec))[0], (n, r)
+
+
+def test_config4_sharded_runner_torchrun():
+    """tools/run_config4.py under torchrun (NCCL process group, one rank on
+    this box): sharding + codec + SSE all-reduce give the oracle's per-frame
+    SSE and global PSNR."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(root, "tools", "run_config4.py"),
+           "--frames", "5", "--height", "64", "--width", "208", "--reps", "1", "--dump"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    f = synth.frames_10bit(range(5), H=64, W=208, workers=1)
+    ref = oc.codec_images(f, "uniform", step=16, bit_depth=10)
+    assert line["sse"] == ref["sse"]
+    P = 5 * 64 * 208
+    assert abs(line["global_psnr_db"] - oc.psnr_from_sse(sum(ref["sse"]), P, 10)) < 1e-9

@@ -1,0 +1,98 @@
+#!/usr/bin/env python
+"""Config 4 end to end on 1..8 GPUs (BASELINE.json configs[3]): 3840x2160
+10-bit frames sharded frame-wise across ranks, fused forward / uniform
+quantisation (Δ = 16) / inverse / SSE on each rank (dct16a_codec), then the
+single exchange of the path — the SUM all-reduce of the per-frame uint64 SSE
+vector over NCCL (paper_1606_05562_b200.parallel.reduce_sse).
+
+Launch: python -m torch.distributed.run --nnodes=1 --nproc-per-node N
+        --master-addr 127.0.0.1 --master-port P tools/run_config4.py [--frames F]
+(or plainly with python for one GPU).  Rank 0 prints one JSON line: global
+PSNR from ΣSSE, the per-frame SSE vector (--dump), codec time as the max over
+ranks (CUDA events), all-reduce time, blocks/s over all ranks.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+
+    import paper_1606_05562_b200 as pkg
+    import synth
+    from paper_1606_05562_b200 import parallel
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--frames", type=int, default=1000)
+    ap.add_argument("--height", type=int, default=2160)
+    ap.add_argument("--width", type=int, default=3840)
+    ap.add_argument("--step", type=int, default=16)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--dump", action="store_true", help="print the per-frame SSE vector")
+    a = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    f0, f1 = parallel.shard(a.frames, world, rank)
+    x = torch.from_numpy(synth.frames_10bit(range(f0, f1), H=a.height, W=a.width, total=1000)).to(dev)
+    n = f1 - f0
+    q = pkg.make_quant("uniform", step=a.step)
+    sse = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    d = pkg.desc_of(x) if n else None
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if n:
+            pkg.dct16a_codec(x, q, sse, None, None, d, stream)
+
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.reps):
+        step()
+    e1.record(stream)
+    e1.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / a.reps], dtype=torch.float64, device=dev)
+    parallel.reduce_sse(sse[:n], f0, a.frames)          # warm the collective (NCCL setup)
+    torch.cuda.synchronize()
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r0.record(stream)
+    full = parallel.reduce_sse(sse[:n], f0, a.frames)
+    r1.record(stream)
+    r1.synchronize()
+    ar_ms = torch.tensor([r0.elapsed_time(r1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ar_ms, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        tot = int(full.sum().item())
+        P = a.frames * a.height * a.width
+        blocks = a.frames * (a.height // 16) * (a.width // 16)
+        line = {"config": 4, "n_gpus": world, "frames": a.frames, "step": a.step,
+                "codec_ms_max_over_ranks": float(ms.item()), "allreduce_ms": float(ar_ms.item()),
+                "blocks_per_s": blocks / (float(ms.item()) / 1e3),
+                "global_psnr_db": parallel.psnr_from_sse(tot, P, 10), "sse_total": tot}
+        if a.dump:
+            line["sse"] = full.cpu().tolist()
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
