@@ -443,3 +443,36 @@ def test_uniform_recon_near_ties_irrational_vs_decimal():
         d = oc._uniform_pixel_decimal(q[b], int(i), int(j), step, prec=80)
         want = int(d.to_integral_value(rounding=decimal.ROUND_HALF_UP))
         assert out["recon"][b, i, j] == min(1023, max(0, want))
+
+
+# ------------------------------------------------------------------ SSIM
+from oracle import quality as oq  # noqa: E402
+
+
+def test_ssim_identity_negative_and_window():
+    img = synth.image_u8(3, 48, 64)
+    assert oq.ssim(img[None], img[None])[0] == pytest.approx(1.0, abs=1e-12)
+    assert oq.ssim(img[None], (255 - img)[None])[0] < 0.5
+    w = oq.gaussian_window()
+    assert abs(w.sum() - 1.0) < 1e-15 and w.shape == (11, 11) and np.allclose(w, w.T)
+    assert np.argmax(w) == 60                       # centre tap (5, 5)
+
+
+def test_ssim_constant_images_closed_form():
+    # constant a vs constant b: σ = 0, so SSIM = (2ab + C1)/(a² + b² + C1) (Wang 2004 eq. 13)
+    C1 = (0.01 * 255) ** 2
+    for a, b in [(10, 200), (128, 129), (0, 255)]:
+        x = np.full((1, 16, 16), a, dtype=np.uint8)
+        y = np.full((1, 16, 16), b, dtype=np.uint8)
+        want = (2 * a * b + C1) / (a * a + b * b + C1)
+        assert oq.ssim(x, y)[0] == pytest.approx(want, abs=1e-12)
+
+
+def test_ssim_against_straight_line_loops():
+    rng = np.random.default_rng(8)
+    x = synth.image_u8(4, 16, 24)
+    y = np.clip(x.astype(int) + rng.integers(-20, 21, size=x.shape), 0, 255).astype(np.uint8)
+    assert oq.ssim(x[None], y[None])[0] == pytest.approx(oq.ssim_bruteforce(x, y), abs=1e-12)
+    f = synth.frame_10bit(3, H=16, W=16)
+    g = np.clip(f.astype(int) + 7, 0, 1023)
+    assert oq.ssim(f[None], g[None], bit_depth=10)[0] == pytest.approx(oq.ssim_bruteforce(f, g, 10), abs=1e-12)
