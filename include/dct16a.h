@@ -144,6 +144,19 @@ DCT16A_API int dct16a_codec(const void* src, const dct16a_desc* desc,
                             uint64_t* sse, double* psnr, void* stream);
 
 /*
+ * dct16a_ssim — mean SSIM per image (Wang et al. 2004):
+ * 11x11 Gaussian window (sigma 1.5, unit sum), K1 = 0.01, K2 = 0.03,
+ * L = 2^b - 1, full resolution, averaged over every window position that lies
+ * inside the first valid_height rows (reading A21).  Computed in float64;
+ * independent of scheduling (fixed-point 2^-32 accumulation of tile sums).
+ *   ref, test : two image batches with the same *desc.
+ *   ssim      : float64 out [batch].
+ * Errors: DCT16A_ESHAPE if valid_height < 11.
+ */
+DCT16A_API int dct16a_ssim(const void* ref, const void* test, const dct16a_desc* desc, double* ssim,
+                           void* stream);
+
+/*
  * dct16a_zonal_sweep — the zonal path of dct16a_codec for every retained
  * count r = r_first .. r_first + r_count - 1 in one pass over the images: the
  * r-sweep of the paper's compression experiment (Figs. 1-2;

@@ -10,7 +10,7 @@ from __future__ import annotations
 
 from ._lib import (OPT_CODEC_PATH, OPT_FWD_STORE, UNIFORM, ZONAL, Dct16aError, Desc, Quant,  # noqa: F401
                    dct16a_codec, dct16a_forward, dct16a_get_option, dct16a_inverse, dct16a_last_error,
-                   dct16a_psnr, dct16a_quantize, dct16a_set_option, dct16a_version, dct16a_zonal_sweep, desc_of, lib,
+                   dct16a_psnr, dct16a_quantize, dct16a_set_option, dct16a_ssim, dct16a_version, dct16a_zonal_sweep, desc_of, lib,
                    make_desc, make_quant)
 
 __version__ = "0.1.0"
@@ -42,6 +42,16 @@ def codec(images, mode="zonal", r=16, step=16, valid_height=None, want_recon=Tru
     recon = torch.empty_like(images) if want_recon else None
     dct16a_codec(images, make_quant(mode, r, step), sse, recon, psnr, d, stream)
     return recon, sse, psnr
+
+
+def ssim(ref, test, bit_depth=None, valid_height=None, stream=None):
+    """Mean SSIM per image of two (batch, H, W) CUDA tensors; float64 [batch]."""
+    import torch
+    if ref.dim() == 2:
+        ref, test = ref.unsqueeze(0), test.unsqueeze(0)
+    out = torch.empty(ref.shape[0], dtype=torch.float64, device=ref.device)
+    dct16a_ssim(ref, test, out, desc_of(ref, bit_depth, valid_height), stream)
+    return out
 
 
 def zonal_sweep(images, r_first=1, r_count=256, valid_height=None, stream=None):

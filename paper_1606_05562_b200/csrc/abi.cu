@@ -217,6 +217,18 @@ DCT16A_API int dct16a_codec(const void* src, const dct16a_desc* desc, const dct1
                     "dct16a_codec");
 }
 
+DCT16A_API int dct16a_ssim(const void* ref, const void* test, const dct16a_desc* desc, double* ssim,
+                           void* stream) {
+    Geom g;
+    int rc;
+    if ((rc = check_desc(desc, &g))) return rc;
+    if ((rc = check_ptr(ref, "ref")) || (rc = check_ptr(test, "test"))) return rc;
+    if (g.VH < 11) return fail(DCT16A_ESHAPE, "valid_height %d < 11 (SSIM window)", g.VH);
+    if (!ssim) return fail(DCT16A_ENULL, "ssim is NULL");
+    if (reinterpret_cast<uintptr_t>(ssim) & 7u) return fail(DCT16A_EALIGN, "ssim is not 8-byte aligned");
+    return launched(launch_ssim(ref, test, g, ssim, static_cast<cudaStream_t>(stream)), "dct16a_ssim");
+}
+
 DCT16A_API int dct16a_zonal_sweep(const void* src, const dct16a_desc* desc, int32_t r_first, int32_t r_count,
                                   uint64_t* sse, double* psnr, void* stream) {
     Geom g;

@@ -43,6 +43,8 @@ int zonal_band(int r);
 // warp-per-block-pair codec (uniform, and zonal cases zonal_tpb does not take)
 int launch_codec_warp(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse,
                       cudaStream_t st);
+// mean SSIM per image (ssim.cu)
+int launch_ssim(const void* ref, const void* test, const Geom& g, double* ssim, cudaStream_t st);
 // zonal r-sweep (sweep.cu) and the shared PSNR finaliser
 int launch_sweep(const void* src, const Geom& g, int r_first, int r_count, uint64_t* sse, double* psnr,
                  cudaStream_t st);

@@ -23,7 +23,7 @@ def declared_symbols():
 def test_library_loads_and_exports_header_symbols():
     L = pkg.lib()
     syms = declared_symbols()
-    assert len(syms) == 10
+    assert len(syms) == 11
     for s in syms:
         assert hasattr(L, s), s
     out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout

@@ -461,3 +461,50 @@ def test_config4_sharded_runner_torchrun():
     assert line["sse"] == ref["sse"]
     P = 5 * 64 * 208
     assert abs(line["global_psnr_db"] - oc.psnr_from_sse(sum(ref["sse"]), P, 10)) < 1e-9
+
+
+# ----------------------------------------------------------------- SSIM
+from oracle import quality as oq  # noqa: E402
+
+
+def test_ssim_kernel_against_oracle():
+    """dct16a_ssim (float64, Wang 2004 defaults) against the oracle's plain
+    sliding-window SSIM: codec reconstructions, 10-bit, valid_height, ragged
+    widths, identical and negated images; |Δ| <= 1e-9."""
+    imgs = np.concatenate([synth.batch_u8([80, 81], 48, 208), synth.adversarial_u8(48, 208)])
+    x = to_dev(imgs)
+    rec, _, _ = pkg.codec(x, "zonal", r=16)
+    torch.cuda.synchronize()
+    got = pkg.ssim(x, rec).cpu().numpy()
+    want = oq.ssim(imgs, rec.cpu().numpy())
+    assert np.max(np.abs(got - want)) < 1e-9
+    assert np.all(pkg.ssim(x, x).cpu().numpy() == 1.0)
+    neg = to_dev(255 - imgs)
+    assert np.max(np.abs(pkg.ssim(x, neg).cpu().numpy() - oq.ssim(imgs, 255 - imgs))) < 1e-9
+    f = synth.frames_10bit([21, 22], H=64, W=144, workers=1)
+    fd = to_dev(f)
+    fr, _, _ = pkg.codec(fd, "uniform", step=16)
+    torch.cuda.synchronize()
+    assert np.max(np.abs(pkg.ssim(fd, fr).cpu().numpy() - oq.ssim(f, fr.cpu().numpy(), 10))) < 1e-9
+    v = synth.video_u8(2, H=40, W=96, pad_to=48, workers=1)
+    vd = to_dev(v)
+    vr, _, _ = pkg.codec(vd, "zonal", r=32, valid_height=40)
+    torch.cuda.synchronize()
+    got = pkg.ssim(vd, vr, valid_height=40).cpu().numpy()
+    assert np.max(np.abs(got - oq.ssim(v, vr.cpu().numpy(), valid_height=40))) < 1e-9
+    t = synth.batch_u8([83], 16, 16)
+    td = to_dev(t)
+    tr_, _, _ = pkg.codec(td, "zonal", r=4)
+    torch.cuda.synchronize()
+    assert abs(float(pkg.ssim(td, tr_)[0]) - oq.ssim(t, tr_.cpu().numpy())[0]) < 1e-9
+
+
+@pytest.mark.slow
+def test_ssim_config1_and_config5_sample():
+    img = synth.image_u8(0)[None]
+    x = to_dev(img)
+    rec, _, _ = pkg.codec(x, "zonal", r=16)
+    torch.cuda.synchronize()
+    got = float(pkg.ssim(x, rec)[0])
+    assert abs(got - oq.ssim(img, rec.cpu().numpy())[0]) < 1e-9
+    assert 0.5 < got < 1.0
