@@ -270,7 +270,7 @@ def run_ours(args):
                            "parallelism": f"dp{world} (independent images, no collective)",
                            "l2": "inputs (1 GiB) and outputs (4 GiB) larger than L2; no flush"},
                 "hbm_gbs": achieved,
-                "roofline": {"kernel": "fwd_kernel<1>", "bound": "hbm", "achieved": achieved, "peak": peak,
+                "roofline": {"kernel": "fwd_kernel<1,5>", "bound": "hbm", "achieved": achieved, "peak": peak,
                              "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                              "traffic": traffic, "alg_bytes_per_launch": alg_bytes},
                 "clocks": clk.summary(),

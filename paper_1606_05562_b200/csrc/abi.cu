@@ -251,7 +251,7 @@ DCT16A_API int dct16a_set_option(int option, int value) {
         return DCT16A_OK;
     }
     if (option == DCT16A_OPT_FWD_STORE) {
-        if (value < -1 || value > 5) return fail(DCT16A_EDOMAIN, "forward store mode %d not in [-1, 5]", value);
+        if (value < -1 || value > 7) return fail(DCT16A_EDOMAIN, "forward store mode %d not in [-1, 7]", value);
         g_fwd_store.store(value);
         return DCT16A_OK;
     }

@@ -18,6 +18,19 @@ import sys, json, torch
 sys.path.insert(0, %r)
 import paper_1606_05562_b200 as pkg, synth
 cfg, frames = %d, %d
+if cfg == 2:
+    x = torch.from_numpy(synth.batch_u8(range(4096), 512, 512)).cuda()
+    coef = torch.empty((4096 * 1024, 16, 16), dtype=torch.int32, device="cuda")
+    d = pkg.desc_of(x)
+    for _ in range(5): pkg.dct16a_forward(x, coef, d)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(100): pkg.dct16a_forward(x, coef, d)
+    b.record(); b.synchronize()
+    ms = a.elapsed_time(b) / 100
+    print(json.dumps({"ms": ms, "GBs": 4096 * 1024 * 1280 / ms / 1e6, "chk": int(coef[12345].sum()) + int(coef[-1].sum())}))
+    sys.exit(0)
 if cfg == 4:
     x = torch.from_numpy(synth.frames_10bit(range(frames))).cuda(); q = pkg.make_quant("uniform", step=16); vh = None
 else:
