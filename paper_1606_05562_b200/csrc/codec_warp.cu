@@ -29,6 +29,7 @@
 //   DC input, pixel = floor((N + 1152.5)/2304) as in zonal_tpb.cu.
 #include <cuda.h>
 #include <stdint.h>
+#include <math.h>
 #include <string.h>
 
 #include <type_traits>
@@ -76,6 +77,7 @@ struct WParams {
     int r;
     // uniform
     int step, F, wbits, hi_shift, hi_c, hi_c2;
+    uint32_t hi_mult;   // 2^hi_shift (an opaque multiplier: one IMAD builds the high word)
     float magic_f, half_delta;
     uint32_t magic_bits;
 };
@@ -161,8 +163,12 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
         fence_mbar_init();
         prefetch_tmap(&tin);
         if (p.has_recon) prefetch_tmap(&tout);
-        for (int s = 0; s < kWStages - 1; ++s)
-            if (t0 + s < t1) w_issue<ELEM>(&tin, p, t0 + s, wbase + s * Cfg::kStageBytes, &bars[s], pol);
+        TileCursor ic;
+        ic.init(p, t0);
+        for (int s = 0; s < kWStages - 1; ++s) {
+            if (t0 + s < t1) w_issue_at<ELEM>(&tin, p, ic, wbase + s * Cfg::kStageBytes, &bars[s], pol);
+            ic.advance(p);
+        }
     }
     __syncwarp();
 
@@ -200,12 +206,14 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
     unsigned long long acc = 0;
     int cur_n = -1;
     int it = 0;
-    for (long long tix = t0; tix < t1; ++tix, ++it) {
+    TileCursor cc, nc;   // the tile being consumed and the one kWStages - 1 ahead (next to issue)
+    cc.init(p, t0);
+    nc.init(p, t0 + kWStages - 1);
+    for (long long tix = t0; tix < t1; ++tix, ++it, cc.advance(p), nc.advance(p)) {
         const int s = it % kWStages;
         uint8_t* stage = wbase + s * Cfg::kStageBytes;
         mbar_wait(&bars[s], (it / kWStages) & 1);
-        int n, by, x0;
-        w_tile_coords<ELEM>(p, tix, &n, &by, &x0);
+        const int n = cc.n, by = cc.by, x0 = cc.x0();
         if (n != cur_n) {
 #pragma unroll
             for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -258,7 +266,7 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
                         const float e = fmaf(fabsf(z[k]), cq[ck], p.half_delta);
                         const uint32_t bits = __float_as_uint(__fadd_rd(e, p.magic_f));
                         nmin = min(nmin, (bits & fmask) | orm[ck]);
-                        const double d = __hiloint2double(static_cast<int>((bits >> p.F) * (1u << p.hi_shift) + p.hi_c2), 0);
+                        const double d = __hiloint2double(static_cast<int>((bits >> p.F) * p.hi_mult + p.hi_c2), 0);
                         const double cm = fma(d, wq[ck], kq[ck]);
                         c[k] = __hiloint2double(__double2hiint(cm) ^ static_cast<int>(__float_as_uint(z[k]) & 0x80000000u),
                                                 __double2loint(cm));
@@ -359,12 +367,12 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
         if (lane == 0) {
             if (p.has_recon) {
                 fence_async_smem();
-                w_store<ELEM>(&tout, p, tix, stage);
+                w_store_at<ELEM>(&tout, p, cc, stage);
                 bulk_commit();
                 bulk_wait_read<1>();   // the store of tile tix-1 has left the stage refilled next
             }
             const long long nt = tix + kWStages - 1;
-            if (nt < t1) w_issue<ELEM>(&tin, p, nt, wbase + ((it + kWStages - 1) % kWStages) * Cfg::kStageBytes,
+            if (nt < t1) w_issue_at<ELEM>(&tin, p, nc, wbase + ((it + kWStages - 1) % kWStages) * Cfg::kStageBytes,
                                        &bars[(it + kWStages - 1) % kWStages], pol);
         }
         __syncwarp();
@@ -423,11 +431,12 @@ int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon
         p.half_delta = hd;
         p.magic_f = 1.5f * static_cast<float>(1 << (23 - p.F));
         memcpy(&p.magic_bits, &p.magic_f, 4);
-        p.wbits = static_cast<int>((delta + 2.0 * err) * (1 << p.F)) + 2;
+        p.wbits = static_cast<int>(ceil((delta + 2.0 * err) * (1 << p.F)));
         // level -> double 1.5·2^E + m: E with 2^E > 2·m_max, m placed at bit (20 - E) of the high word
         int E = 1;
         while ((1 << E) <= 2 * (static_cast<int>(e_max) + 1)) ++E;
         p.hi_shift = 20 - E;
+        p.hi_mult = 1u << p.hi_shift;
         p.hi_c = 0x3FF00000 + ((E) << 20) + (1 << 19);   // high word of 1.5·2^E
         // the same word from bits >> F = (magic_bits >> F) + m (arithmetic mod 2^32)
         p.hi_c2 = static_cast<int>(static_cast<uint32_t>(p.hi_c) - ((p.magic_bits >> p.F) << p.hi_shift));

@@ -105,8 +105,12 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
         for (int s = 0; s < kSStages; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
         prefetch_tmap(&tin);
-        for (int s = 0; s < kSStages - 1; ++s)
-            if (t0 + s < t1) w_issue<ELEM>(&tin, p, t0 + s, wbase + s * Cfg::kStageBytes, &bars[s], pol);
+        TileCursor ic;
+        ic.init(p, t0);
+        for (int s = 0; s < kSStages - 1; ++s) {
+            if (t0 + s < t1) w_issue_at<ELEM>(&tin, p, ic, wbase + s * Cfg::kStageBytes, &bars[s], pol);
+            ic.advance(p);
+        }
     }
     __syncthreads();
 
@@ -120,12 +124,14 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
 
     int cur_n = -1;
     int it = 0;
-    for (long long tix = t0; tix < t1; ++tix, ++it) {
+    TileCursor cc, nc;   // the tile being consumed and the one kSStages - 1 ahead (next to issue)
+    cc.init(p, t0);
+    nc.init(p, t0 + kSStages - 1);
+    for (long long tix = t0; tix < t1; ++tix, ++it, cc.advance(p), nc.advance(p)) {
         const int s = it % kSStages;
         uint8_t* stage = wbase + s * Cfg::kStageBytes;
         mbar_wait(&bars[s], (it / kSStages) & 1);
-        int n, by, x0;
-        w_tile_coords<ELEM>(p, tix, &n, &by, &x0);
+        const int n = cc.n, by = cc.by, x0 = cc.x0();
         if (n != cur_n) {   // flush the per-r SSE of the previous image (warp-uniform)
             __syncwarp();
             if (cur_n >= 0)
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
         }
         if (lane == 0) {
             const long long nt = tix + kSStages - 1;
-            if (nt < t1) w_issue<ELEM>(&tin, p, nt, wbase + ((it + kSStages - 1) % kSStages) * Cfg::kStageBytes,
+            if (nt < t1) w_issue_at<ELEM>(&tin, p, nc, wbase + ((it + kSStages - 1) % kSStages) * Cfg::kStageBytes,
                                        &bars[(it + kSStages - 1) % kSStages], pol);
         }
         __syncwarp();

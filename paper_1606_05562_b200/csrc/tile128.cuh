@@ -32,6 +32,47 @@ __device__ __forceinline__ void w_tile_coords(const P& p, long long tix, int* n,
     *x0 = tb * kWTile * 16;
 }
 
+// Tile coordinates advanced incrementally (a warp walks a contiguous tile range):
+// one division at the start instead of two 64-bit divisions per tile.
+struct TileCursor {
+    int n, by, tb;
+    template <class P>
+    __device__ __forceinline__ void init(const P& p, long long tix) {
+        int x0;
+        w_tile_coords<1>(p, tix, &n, &by, &x0);
+        tb = x0 / (kWTile * 16);
+    }
+    template <class P>
+    __device__ __forceinline__ void advance(const P& p) {
+        if (++tb == p.tiles_per_strip) {
+            tb = 0;
+            if (++by == p.BY) {
+                by = 0;
+                ++n;
+            }
+        }
+    }
+    __device__ __forceinline__ int x0() const { return tb * kWTile * 16; }
+};
+
+template <int ELEM, class P>
+__device__ __forceinline__ void w_issue_at(const CUtensorMap* tin, const P& p, const TileCursor& c, uint8_t* stage,
+                                           uint64_t* bar, uint64_t pol) {
+    constexpr int box_px = 128 / ELEM;
+    const int x0 = c.x0();
+    const int nbox = (ELEM == 2 && x0 + box_px < p.W) ? 2 : 1;
+    mbar_arrive_expect_tx(bar, static_cast<uint32_t>(nbox * 2048));
+    for (int h = 0; h < nbox; ++h) tma_load_3d(stage + h * 2048, tin, bar, x0 + h * box_px, c.by * 16, c.n, pol);
+}
+
+template <int ELEM, class P>
+__device__ __forceinline__ void w_store_at(const CUtensorMap* tout, const P& p, const TileCursor& c, uint8_t* stage) {
+    constexpr int box_px = 128 / ELEM;
+    const int x0 = c.x0();
+    const int nbox = (ELEM == 2 && x0 + box_px < p.W) ? 2 : 1;
+    for (int h = 0; h < nbox; ++h) tma_store_3d(tout, stage + h * 2048, x0 + h * box_px, c.by * 16, c.n);
+}
+
 template <int ELEM, class P>
 __device__ __forceinline__ void w_issue(const CUtensorMap* tin, const P& p, long long tix, uint8_t* stage,
                                         uint64_t* bar, uint64_t pol) {
