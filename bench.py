@@ -183,18 +183,11 @@ def run_ours(args):
     # Generation is split across ranks (rank r draws seeds r, r+world, ...) and
     # all-gathered once before timing, so N ranks do not each regenerate 1 GiB.
     if world > 1:
-        mine = list(range(rank, N_IMG, world))
+        from paper_1606_05562_b200 import parallel
+        mine = parallel.strided_ids(N_IMG, world, rank)
         part = torch.from_numpy(synth.batch_u8(mine, H, W, workers=max(1, host_cores() // world))).to(dev)
-        m = (N_IMG + world - 1) // world
-        buf = torch.zeros((m, H, W), dtype=torch.uint8, device=dev)
-        buf[:part.shape[0]] = part
-        parts = [torch.empty_like(buf) for _ in range(world)]
-        dist.all_gather(parts, buf)
-        x = torch.empty((N_IMG, H, W), dtype=torch.uint8, device=dev)
-        for r in range(world):
-            cnt = len(range(r, N_IMG, world))
-            x[r::world] = parts[r][:cnt]
-        del parts, buf, part
+        x = parallel.allgather_strided(part, N_IMG, world)
+        del part
         host = x.cpu().pin_memory()
     else:
         host = torch.from_numpy(synth.batch_u8(range(N_IMG), H, W)).pin_memory()

@@ -55,3 +55,29 @@ def codec_sharded(local_frames, offset: int, n_total: int, mode: str = "uniform"
     bits = 8 if local_frames.element_size() == 1 else 10
     total = int(full.sum().item())
     return recon, full, psnr_from_sse(total, n_total * vh * w, bits)
+
+
+def strided_ids(n_items: int, world: int, rank: int) -> list[int]:
+    """Items r, r + world, r + 2·world, ... — the ids rank `rank` generates when
+    every rank needs the whole batch (weak-scaling bench inputs)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    return list(range(rank, n_items, world))
+
+
+def allgather_strided(part, n_items: int, world: int, group=None):
+    """Reassemble the full batch from every rank's strided part (part = items
+    rank, rank + world, ...; shape (len, ...)) with one all_gather of equal-size
+    padded buffers; returns the (n_items, ...) tensor in item order on every rank."""
+    import torch
+    import torch.distributed as dist
+    m = (n_items + world - 1) // world
+    buf = torch.zeros((m, *part.shape[1:]), dtype=part.dtype, device=part.device)
+    buf[:part.shape[0]] = part
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    out = torch.empty((n_items, *part.shape[1:]), dtype=part.dtype, device=part.device)
+    for r in range(world):
+        cnt = len(range(r, n_items, world))
+        out[r::world] = parts[r][:cnt]
+    return out

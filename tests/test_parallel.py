@@ -64,3 +64,32 @@ def test_sse_allreduce_gloo(world, n_total):
     want = [(f * 7919) % 100003 + 2 ** 40 for f in range(n_total)]
     for r in range(world):
         assert out[r] == want          # every rank holds every frame's SSE, exactly
+
+
+def _gather_worker(rank, world, port, n_total, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ids = parallel.strided_ids(n_total, world, rank)
+    part = torch.tensor([[i * 10 + j for j in range(3)] for i in ids], dtype=torch.int64).reshape(len(ids), 3)
+    full = parallel.allgather_strided(part, n_total, world)
+    out[rank] = full.tolist()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_total", [(2, 7), (2, 8), (3, 10)])
+def test_allgather_strided_gloo(world, n_total):
+    """bench.py's input assembly: each rank generates items rank::world, one
+    all_gather rebuilds the batch in item order on every rank."""
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, n_total, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    want = [[i * 10 + j for j in range(3)] for i in range(n_total)]
+    for r in range(world):
+        assert out[r] == want
