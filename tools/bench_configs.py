@@ -1,6 +1,9 @@
-"""Per-config throughput of the fused codec path (configs 1, 3, 4) and the
-forward kernel (config 2), device-resident inputs, CUDA events.  Prints one
-JSON object per config.  Secondary measurements (bench.py times config 2)."""
+"""Per-config throughput of every hot-path entry on B200: the forward kernel
+(config 2), the fused codec (configs 1, 3, 4) and the r-sweep (config 5),
+device-resident inputs, CUDA events; beside each, the CPU oracle (as it
+stands, numpy float64 / exact integers, one process per host core) on a
+bounded sample of the same workload.  One JSON object per config.  Secondary
+measurements: bench.py times config 2 under the driver contract."""
 import argparse
 import json
 import os
@@ -10,6 +13,7 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_1606_05562_b200 as pkg  # noqa: E402
@@ -27,6 +31,46 @@ def timeit(fn, reps, warm=3):
     b.record()
     b.synchronize()
     return a.elapsed_time(b) / reps
+
+
+CORES = len(os.sched_getaffinity(0))
+
+
+def oracle_items(c):
+    return {1: 1, 2: 1024, 3: 32, 4: 16, 5: 16}[c]
+
+
+def _oracle_job(args):
+    from threadpoolctl import threadpool_limits
+
+    from oracle import codec as oc
+    c, img, kw, vh = args
+    with threadpool_limits(1):
+        if c == 2:
+            oc.forward(oc.to_blocks(img.astype(np.int64)))
+        elif c == 5:
+            for r in range(1, 257):
+                oc.codec_images(img, "zonal", r=r)
+        else:
+            oc.codec_images(img, kw["mode"], r=kw.get("r", 16), step=kw.get("step", 16),
+                            bit_depth=10 if kw["mode"] == "uniform" else 8, valid_height=vh)
+    n, h, w = img.shape
+    return n * (h // 16) * (w // 16) * (256 if c == 5 else 1)
+
+
+def oracle_rate(c, xs, kw, vh):
+    """The oracle as it stands on a bounded sample (one image/frame per job,
+    one process per host core); returns (units/s over wall time, description)."""
+    from concurrent.futures import ProcessPoolExecutor
+    jobs = [(c, xs[i:i + 1], kw, vh) for i in range(xs.shape[0])]
+    with ProcessPoolExecutor(min(CORES, len(jobs))) as ex:
+        list(ex.map(_oracle_job, [(c, xs[:1, :16, :16], kw, None)] * min(CORES, len(jobs))))   # warm the workers
+        t0 = time.time()
+        units = sum(ex.map(_oracle_job, jobs))
+        wall = time.time() - t0
+    what = {1: "config-1 image", 2: "1024 config-2 images", 3: "32 config-3 frames", 4: "16 config-4 frames",
+            5: "16 config-5 images x 256 r"}[c]
+    return units / wall, f"{what}, {min(CORES, len(jobs))} processes, {wall:.1f} s wall"
 
 
 def main():
@@ -83,9 +127,15 @@ def main():
             ps = torch.empty(n, dtype=torch.float64, device="cuda")
             ms = timeit(lambda: pkg.dct16a_codec(x, q, sse, recon, ps, d), args.reps)
             alg = blocks * 2 * 256 * x.element_size()
+        xs = x[:oracle_items(c)].cpu().numpy()
+        o_rate, o_sample = oracle_rate(c, xs, kw if c in (1, 3, 4) else None, vh if c in (1, 3, 4) else None)
+        gpu_rate = (blocks * 256 if c == 5 else blocks) / ms * 1e3
         print(json.dumps({"config": c, "blocks": blocks, "ms": ms, "blocks_per_s": blocks / ms * 1e3,
                           "alg_GBs": alg / ms / 1e6, "frac_of_measured_hbm": alg / ms / 1e6 / peak,
-                          "gen_s": round(gen_s, 1), **extra}), flush=True)
+                          "gen_s": round(gen_s, 1), **extra,
+                          "oracle": {"rate": o_rate, "unit": "block-evaluations/s" if c == 5 else "blocks/s",
+                                     "sample": o_sample, "cores": CORES},
+                          "gpu_over_oracle": gpu_rate / o_rate}), flush=True)
         del x
         torch.cuda.empty_cache()
 
