@@ -94,6 +94,17 @@ DCT16A_API int dct16a_forward(const void* src, const dct16a_desc* desc,
                               int32_t* coef, void* stream);
 
 /*
+ * dct16a_forward16 — the same Z = T·X·Tᵀ for 8-bit images, stored in 16 bits
+ * (SURVEY.md §8(f) f4): every AC coefficient fits int16 (|Z| <= 32640) and
+ * Z_00 = block sum fits uint16 ([0, 65280]).  coef16[b·256 + 16·k + l] holds the
+ * low 16 bits of Z: read the DC entry (k = l = 0) as uint16 and every other
+ * entry as int16.  Half the output bytes of dct16a_forward.
+ * Errors: DCT16A_EDOMAIN unless bit_depth = 8.
+ */
+DCT16A_API int dct16a_forward16(const void* src, const dct16a_desc* desc, int16_t* coef16,
+                                void* stream);
+
+/*
  * dct16a_quantize — the quantisation stage with S folded in.
  *   coef   : int32 block-major Z as written by dct16a_forward.
  *   qcoef  : int32 out, same shape.  Zonal: Z ⊙ M_r (M_r = first r zig-zag

@@ -9,7 +9,7 @@ memory, streams and process groups only.
 from __future__ import annotations
 
 from ._lib import (OPT_CODEC_PATH, OPT_FWD_STORE, UNIFORM, ZONAL, Dct16aError, Desc, Quant,  # noqa: F401
-                   dct16a_codec, dct16a_forward, dct16a_get_option, dct16a_inverse, dct16a_last_error,
+                   dct16a_codec, dct16a_forward, dct16a_forward16, dct16a_get_option, dct16a_inverse, dct16a_last_error,
                    dct16a_psnr, dct16a_quantize, dct16a_set_option, dct16a_ssim, dct16a_version, dct16a_zonal_sweep, desc_of, lib,
                    make_desc, make_quant)
 
@@ -26,6 +26,20 @@ def forward(images, out=None, stream=None):
     if out is None:
         out = torch.empty((n * (h // 16) * (w // 16), 16, 16), dtype=torch.int32, device=images.device)
     dct16a_forward(images, out, desc_of(images), stream)
+    return out
+
+
+def forward16(images, out=None, stream=None):
+    """Z = T·X·Tᵀ of 8-bit images stored in 16 bits: int16 (batch·H/16·W/16,
+    16, 16) block-major; entry [:, 0, 0] is the block sum as uint16 bits
+    (use `.view(torch.uint16)` or `& 0xFFFF` on it), every other entry is int16."""
+    import torch
+    if images.dim() == 2:
+        images = images.unsqueeze(0)
+    n, h, w = images.shape
+    if out is None:
+        out = torch.empty((n * (h // 16) * (w // 16), 16, 16), dtype=torch.int16, device=images.device)
+    dct16a_forward16(images, out, desc_of(images), stream)
     return out
 
 

@@ -59,6 +59,8 @@ def lib() -> ctypes.CDLL:
         L.dct16a_codec.argtypes = [vp, P(Desc), P(Quant), vp, vp, vp, vp]
         for f in ("dct16a_forward", "dct16a_quantize", "dct16a_inverse", "dct16a_psnr", "dct16a_codec"):
             getattr(L, f).restype = ctypes.c_int
+        L.dct16a_forward16.argtypes = [vp, P(Desc), vp, vp]
+        L.dct16a_forward16.restype = ctypes.c_int
         L.dct16a_ssim.argtypes = [vp, vp, P(Desc), vp, vp]
         L.dct16a_ssim.restype = ctypes.c_int
         L.dct16a_zonal_sweep.argtypes = [vp, P(Desc), ctypes.c_int32, ctypes.c_int32, vp, vp, vp]
@@ -147,6 +149,11 @@ def dct16a_codec(src, quant: Quant, sse, recon=None, psnr=None, desc: Desc | Non
     d = desc if desc is not None else desc_of(src)
     _check(lib().dct16a_codec(_ptr(src), ctypes.byref(d), ctypes.byref(quant), _ptr(recon), _ptr(sse),
                               _ptr(psnr), _stream(stream)))
+
+
+def dct16a_forward16(src, coef16, desc: Desc | None = None, stream=None) -> None:
+    d = desc if desc is not None else desc_of(src)
+    _check(lib().dct16a_forward16(_ptr(src), ctypes.byref(d), _ptr(coef16), _stream(stream)))
 
 
 def dct16a_ssim(ref, test, ssim, desc: Desc | None = None, stream=None) -> None:

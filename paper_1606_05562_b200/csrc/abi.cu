@@ -169,6 +169,15 @@ DCT16A_API int dct16a_forward(const void* src, const dct16a_desc* desc, int32_t*
     return launched(launch_forward(src, g, coef, static_cast<cudaStream_t>(stream)), "dct16a_forward");
 }
 
+DCT16A_API int dct16a_forward16(const void* src, const dct16a_desc* desc, int16_t* coef16, void* stream) {
+    Geom g;
+    int rc;
+    if ((rc = check_desc(desc, &g))) return rc;
+    if (g.bits != 8) return fail(DCT16A_EDOMAIN, "dct16a_forward16 needs 8-bit images (10-bit Z exceeds 16 bits)");
+    if ((rc = check_ptr(src, "src")) || (rc = check_ptr(coef16, "coef16"))) return rc;
+    return launched(launch_forward16(src, g, coef16, static_cast<cudaStream_t>(stream)), "dct16a_forward16");
+}
+
 DCT16A_API int dct16a_quantize(const int32_t* coef, const dct16a_desc* desc, const dct16a_quant* quant,
                                int32_t* qcoef, float* scaled, void* stream) {
     Geom g;

@@ -45,11 +45,14 @@ constexpr int kTile = 32;    // blocks per warp tile = lanes
 //  5: TMA tensor store of the whole tile (8 row pairs, 32 KB), 1 buffer
 //  6: as 5 with 2 buffers (2 warps per SM)
 //  7: as 5 with a 3-stage input ring
+//  8: 16-bit coefficients (dct16a_forward16): the whole tile (32 blocks x
+//     512 B = 16 KB) in one TMA tensor store, 64-byte swizzle, 1 buffer
 template <int SM>
 struct StoreCfg {
-    static constexpr int kBufs = SM == 1 ? 4 : ((SM == 2 || SM == 5 || SM == 7) ? 1 : 2);
+    static constexpr bool kOut16 = SM == 8;
+    static constexpr int kBufs = SM == 1 ? 4 : ((SM == 2 || SM == 5 || SM == 7 || SM == 8) ? 1 : 2);
     static constexpr int kPairs = SM == 3 ? 2 : (SM == 4 ? 4 : (SM >= 5 ? 8 : 1));   // row pairs per store
-    static constexpr int kBytes = kTile * 128 * kPairs;
+    static constexpr int kBytes = kTile * (kOut16 ? 64 : 128) * kPairs;
     static constexpr int kStages = SM == 7 ? 3 : 2;   // input ring depth per warp
 };
 
@@ -221,6 +224,7 @@ __global__ void __launch_bounds__(FwdCfg<ELEM, SM>::kWarps * 32, FwdCfg<ELEM, SM
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             int32_t z0[16], z1[16];   // rows 2r and 2r+1 of Z
+            uint32_t w16[16];         // the same two rows as int16 pairs (store mode 8)
             if constexpr (ELEM == 1) {
                 uint32_t x[16], y[16];
 #pragma unroll
@@ -230,8 +234,20 @@ __global__ void __launch_bounds__(FwdCfg<ELEM, SM>::kWarps * 32, FwdCfg<ELEM, SM
                 }
                 net_fwd(x, y);
                 y[0] -= 0x00080000u;   // remove 16 x (2^15 + 2^31) bias of output l = 0
+                if constexpr (SC::kOut16) {
+                    // y[l] = Z[2r][l] + 2^16·Z[2r+1][l] (mod 2^32) with the low field in int16
+                    // (Z_00 in uint16, no borrow): the int16 rows are the low halves and,
+                    // after undoing the borrow, the high halves
 #pragma unroll
-                for (int l = 0; l < 16; ++l) {
+                    for (int q = 0; q < 8; ++q) {
+                        const uint32_t h0 = (r == 0 && q == 0) ? y[0] : y[2 * q] + 0x8000u;
+                        const uint32_t h1 = y[2 * q + 1] + 0x8000u;
+                        w16[q] = __byte_perm(y[2 * q], y[2 * q + 1], 0x5410);
+                        w16[8 + q] = __byte_perm(h0, h1, 0x7632);
+                    }
+                }
+#pragma unroll
+                for (int l = 0; l < 16 && !SC::kOut16; ++l) {
                     int32_t lo;
                     if (r == 0 && l == 0) lo = static_cast<int32_t>(y[l] & 0xFFFFu);   // Z_00 in [0, 65280]
                     else lo = static_cast<int32_t>(static_cast<int16_t>(y[l] & 0xFFFFu));
@@ -259,10 +275,22 @@ __global__ void __launch_bounds__(FwdCfg<ELEM, SM>::kWarps * 32, FwdCfg<ELEM, SM
             }
             __syncwarp();
             uint8_t* buf = outb + obuf * SC::kBytes;
+            if constexpr (SC::kOut16) {
+                // staging row (64 B) of this lane inside the box {32 int16, box_b blocks, 8}:
+                // 64-byte swizzle, chunk ^= (address >> 7) & 3
+                uint8_t* ob = buf + (half * box_b + lane) * 64;
+                const int sw = (smem_addr(ob) >> 7) & 3;
+                if (lane < box_b) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        *reinterpret_cast<uint4*>(ob + ((c ^ sw) << 4)) =
+                            make_uint4(w16[4 * c], w16[4 * c + 1], w16[4 * c + 2], w16[4 * c + 3]);
+                }
+            }
             // staging row of this lane inside the TMA box {32 ints, box_b blocks, kPairs}
             uint8_t* ob = buf + (half * box_b + lane) * 128;
             const int sw = (smem_addr(ob) >> 7) & 7;   // 128-byte swizzle: chunk ^= row & 7
-            if (SM == 2 || lane < box_b) {
+            if (!SC::kOut16 && (SM == 2 || lane < box_b)) {
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
                     *reinterpret_cast<int4*>(ob + ((c ^ sw) << 4)) =
@@ -322,7 +350,15 @@ int launch_fwd_t(const void* src, const Geom& g, int32_t* coef, cudaStream_t st)
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
         if (rc) return DCT16A_ECUDA;
     }
-    {
+    if (StoreCfg<SM>::kOut16) {
+        // int16 coef viewed as {32 int16 of a row pair, block column bx, row pair, strip}
+        const uint64_t dims[4] = {32u, uint64_t(g.BX), 8u, uint64_t(g.N) * uint64_t(g.BY)};
+        const uint64_t strides[3] = {512u, 64u, uint64_t(g.BX) * 512u};
+        const uint32_t box[4] = {32u, uint32_t(g.BX < 32 ? g.BX : 32), 8u, 1u};
+        int rc = encode_tiled(&tout, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, coef, dims, strides, box,
+                              CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+        if (rc) return DCT16A_ECUDA;
+    } else {
         // coef viewed as {32 int32 of a row pair, block column bx, row pair, strip}
         const uint64_t dims[4] = {32u, uint64_t(g.BX), 8u, uint64_t(g.N) * uint64_t(g.BY)};
         const uint64_t strides[3] = {1024u, 128u, uint64_t(g.BX) * 1024u};
@@ -381,6 +417,12 @@ int launch_fwd_e(const void* src, const Geom& g, int32_t* coef, cudaStream_t st)
 
 int launch_forward(const void* src, const Geom& g, int32_t* coef, cudaStream_t st) {
     return g.elem == 1 ? launch_fwd_e<1>(src, g, coef, st) : launch_fwd_e<2>(src, g, coef, st);
+}
+
+// 16-bit coefficients, 8-bit images only (every Z fits 16 bits: AC in int16,
+// Z_00 in [0, 65280] as uint16 — SURVEY V9, next item f4)
+int launch_forward16(const void* src, const Geom& g, int16_t* coef, cudaStream_t st) {
+    return launch_fwd_t<1, 8>(src, g, reinterpret_cast<int32_t*>(coef), st);
 }
 
 }  // namespace dct16a

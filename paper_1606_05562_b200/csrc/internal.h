@@ -29,6 +29,7 @@ int num_sms();
 // Launchers: return cudaError_t of the launch (cudaSuccess = 0) or a negative
 // DCT16A_E* code for encode failures.
 int launch_forward(const void* src, const Geom& g, int32_t* coef, cudaStream_t st);
+int launch_forward16(const void* src, const Geom& g, int16_t* coef, cudaStream_t st);
 int launch_quantize(const int32_t* coef, const Geom& g, const dct16a_quant& q, int32_t* qcoef,
                     float* scaled, cudaStream_t st);
 int launch_inverse(const int32_t* qcoef, const Geom& g, const dct16a_quant& q, void* recon,

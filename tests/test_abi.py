@@ -23,7 +23,7 @@ def declared_symbols():
 def test_library_loads_and_exports_header_symbols():
     L = pkg.lib()
     syms = declared_symbols()
-    assert len(syms) == 11
+    assert len(syms) == 12
     for s in syms:
         assert hasattr(L, s), s
     out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
@@ -130,3 +130,10 @@ def test_zonal_sweep_validation():
     assert L.dct16a_zonal_sweep(buf, ctypes.byref(d), 1, 256, None, None, None) == -1
     assert L.dct16a_zonal_sweep(buf, ctypes.byref(d), 1, 256, ctypes.c_void_p((1 << 20) + 4), None, None) == -4
     del torch
+
+
+def test_forward16_rejects_10bit():
+    L = pkg.lib()
+    d = pkg.make_desc(64, 64, 1, 10)
+    buf = ctypes.c_void_p(1 << 20)
+    assert L.dct16a_forward16(buf, ctypes.byref(d), buf, None) == -5

@@ -55,6 +55,18 @@ def test_forward_u8_bit_exact(name, imgs):
     assert np.array_equal(gpu_Z(to_dev(imgs)), oracle_Z(imgs))
 
 
+@pytest.mark.parametrize("name,imgs", list(u8_cases()), ids=lambda v: v if isinstance(v, str) else "")
+def test_forward16_bit_exact(name, imgs):
+    """dct16a_forward16: the low 16 bits of Z (DC as uint16, AC as int16)."""
+    x = to_dev(imgs)
+    got = pkg.forward16(x).cpu().numpy().astype(np.int64)
+    Z = oracle_Z(imgs)
+    want = Z.copy()
+    want[:, 0, 0] = Z[:, 0, 0] - 65536 * (Z[:, 0, 0] >= 32768)   # uint16 bits read as int16
+    assert np.array_equal(got, want)
+    assert np.all(np.abs(Z[:, 1:, :]) <= 32767) and np.all(np.abs(Z[:, 0, 1:]) <= 32767)
+
+
 def test_forward_10bit_bit_exact():
     imgs = synth.frames_10bit([0, 1], H=64, W=272, workers=1)
     adv = synth.adversarial_u8(48, 80, bit_depth=10)
