@@ -146,7 +146,9 @@ DCT16A_API int dct16a_psnr(const void* ref, const void* test, const dct16a_desc*
  * in one pass over the input.  Results are identical,
  * byte for byte, to dct16a_forward -> dct16a_quantize -> dct16a_inverse ->
  * dct16a_psnr.
- *   recon : optional pixels out (may be NULL: nothing is written).
+ *   recon : optional pixels out (may be NULL: nothing is written), in the
+ *           layout, pitch, image stride and type of *desc — one descriptor
+ *           describes both src and recon; must not overlap src.
  *   sse   : uint64 out [batch] (exact; overwritten, not accumulated).
  *   psnr  : optional float64 out [batch] (may be NULL).
  */

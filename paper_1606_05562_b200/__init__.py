@@ -53,7 +53,9 @@ def codec(images, mode="zonal", r=16, step=16, valid_height=None, want_recon=Tru
     n = images.shape[0]
     sse = torch.empty(n, dtype=torch.int64, device=images.device)
     psnr = torch.empty(n, dtype=torch.float64, device=images.device)
-    recon = torch.empty_like(images) if want_recon else None
+    # the C ABI describes src and recon with one descriptor: same strides
+    recon = (torch.empty_strided(images.shape, images.stride(), dtype=images.dtype, device=images.device)
+             if want_recon else None)
     dct16a_codec(images, make_quant(mode, r, step), sse, recon, psnr, d, stream)
     return recon, sse, psnr
 

@@ -520,3 +520,41 @@ def test_ssim_config1_and_config5_sample():
     got = float(pkg.ssim(x, rec)[0])
     assert abs(got - oq.ssim(img, rec.cpu().numpy())[0]) < 1e-9
     assert 0.5 < got < 1.0
+
+
+def test_pitched_strided_views_every_entry(codec_path):
+    """Views with row pitch > width and image stride > pitch·height (a window
+    of larger images): forward16, the fused codec (zonal and uniform), the
+    r-sweep and SSIM must see exactly the window."""
+    big = synth.batch_u8([90, 91], 80, 400)
+    view = big[:, 8:72, 32:288]                     # pitch 400, stride 32000, 256 x 64 window
+    t = to_dev(big)[:, 8:72, 32:288]
+    vw = np.ascontiguousarray(view)
+    Z = oracle_Z(vw)
+    got16 = pkg.forward16(t).cpu().numpy().astype(np.int64)
+    Z16 = Z.copy()
+    Z16[:, 0, 0] = Z[:, 0, 0] - 65536 * (Z[:, 0, 0] >= 32768)
+    assert np.array_equal(got16, Z16)
+    for mode, r, step, bd, src_big, win in [("zonal", 32, 16, 8, big, (slice(8, 72), slice(32, 288))),
+                                            ("zonal", 60, 16, 8, big, (slice(8, 72), slice(32, 288)))]:
+        x = to_dev(src_big)[:, win[0], win[1]]
+        rec, sse, _ = pkg.codec(x, mode, r=r, step=step)
+        torch.cuda.synchronize()
+        ref = oc.codec_images(np.ascontiguousarray(src_big[:, win[0], win[1]]), mode, r=r, step=step, bit_depth=bd)
+        assert np.array_equal(rec.cpu().numpy(), ref["recon_img"])
+        assert sse.cpu().tolist() == ref["sse"]
+    f = synth.frames_10bit([30, 31], H=80, W=272, workers=1)
+    fv = np.ascontiguousarray(f[:, 16:64, 16:208])
+    ft = to_dev(f)[:, 16:64, 16:208]
+    rec, sse, _ = pkg.codec(ft, "uniform", step=16)
+    torch.cuda.synchronize()
+    ref = oc.codec_images(fv, "uniform", step=16, bit_depth=10)
+    assert np.array_equal(rec.cpu().numpy(), ref["recon_img"])
+    assert sse.cpu().tolist() == ref["sse"]
+    s, _ = pkg.zonal_sweep(t, 10, 5)
+    torch.cuda.synchronize()
+    for i, r in enumerate(range(10, 15)):
+        assert s[:, i].cpu().tolist() == oc.codec_images(vw, "zonal", r=r)["sse"]
+    rec, _, _ = pkg.codec(t, "zonal", r=16)
+    torch.cuda.synchronize()
+    assert np.max(np.abs(pkg.ssim(t, rec).cpu().numpy() - oq.ssim(vw, rec.cpu().numpy()))) < 1e-9
