@@ -25,6 +25,7 @@
 #include "internal.h"
 #include "net16.cuh"
 #include "ptx.cuh"
+#include "quant.cuh"
 #include "tables.cuh"
 #include "tile128.cuh"
 
@@ -150,10 +151,15 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
             const bool contributes = bb < nb && row_valid;
             int a0, a1;
             row_addr<ELEM>(bb, t, &a0, &a1);
-            float xs[16];   // 2^23 + x[i][j], the SSE reference in the magic-float domain
+            float xs[16];          // 10-bit: 2^23 + x[i][j], the SSE reference in the magic-float domain
+            uint32_t xw[4];        // 8-bit: the packed original row (vabsdiff4/dp4a reference)
             {
                 uint32_t w[4 * ELEM];
                 load_px<ELEM>(stage, a0, a1, w);
+                if (ELEM == 1) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) xw[q] = w[q];
+                }
                 float x[16], y[16];
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
@@ -195,15 +201,34 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
                     N[4 * q + 3] = fmaf(sv, tq.w, N[4 * q + 3]);
                 }
                 if (r >= p.r_first) {
-                    float e = 0.0f;
+                    unsigned ei;
+                    if (ELEM == 1) {
+                        // floor((N + 1152.5)/2304) by one round-down FMA onto 2^23 (exact, see
+                        // header); cvt.pack.sat clamps to [0, 255] and packs 4 pixels, then
+                        // vabsdiff4 + dp4a square and sum against the original bytes
+                        ei = 0;
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        // floor((N + 1152.5)/2304) + 2^23 by one round-down FMA (exact, see header)
-                        const float f = fminf(fmaxf(__fmaf_rd(N[j], inv2304, 8388608.0f), 8388608.0f), top);
-                        const float d = f - xs[j];
-                        e = fmaf(d, d, e);
+                        for (int q = 0; q < 4; ++q) {
+                            int v[4];
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                v[i] = static_cast<int>(__float_as_uint(__fmaf_rd(N[4 * q + i], inv2304, 8388608.0f)) -
+                                                        0x4B000000u);
+                            const uint32_t pk = pack2_sat_u8(v[1], v[0], pack2_sat_u8(v[3], v[2], 0u));
+                            const uint32_t d = __vabsdiffu4(pk, xw[q]);
+                            ei = __dp4a(d, d, ei);
+                        }
+                    } else {
+                        float e = 0.0f;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const float f = fminf(fmaxf(__fmaf_rd(N[j], inv2304, 8388608.0f), 8388608.0f), top);
+                            const float d = f - xs[j];
+                            e = fmaf(d, d, e);
+                        }
+                        ei = __float2uint_rn(e);
                     }
-                    const unsigned tot = __reduce_add_sync(0xffffffffu, contributes ? __float2uint_rn(e) : 0u);
+                    const unsigned tot = __reduce_add_sync(0xffffffffu, contributes ? ei : 0u);
                     if (lane == 0 && tot) atomicAdd(&ssew[r - p.r_first], static_cast<unsigned long long>(tot));
                 }
             }
