@@ -89,6 +89,10 @@ typedef struct dct16a_quant {
  *   src  : image batch laid out as described by *desc (uint8 or int16).
  *   coef : int32 output, batch·BY·BX·256 entries, block-major (see above).
  * Integer-exact.  |Z| <= 65280 (8-bit) / 261888 (10-bit).
+ * Scheduling: the kernel hands out tiles from one of 64 device-side counters
+ * used round-robin by successive calls (a compact write window);
+ * at most 64 dct16a_forward / dct16a_forward16 launches may be executing at
+ * the same time (on any streams) per device.
  */
 DCT16A_API int dct16a_forward(const void* src, const dct16a_desc* desc,
                               int32_t* coef, void* stream);

@@ -303,8 +303,9 @@ __global__ void __launch_bounds__(CodecCfg<UNIFORM>::kWarps * 32) codec_kernel(c
 // ------------------------------------------------------------------ K6
 __global__ void sse_kernel(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b,
                            unsigned long long* sse, const Geom g) {
-    const int n = blockIdx.y;
     const int cpr = g.W * g.elem / 16;   // 16-byte chunks per row
+    __shared__ uint64_t ws[32];
+    for (int n = blockIdx.y; n < g.N; n += gridDim.y) {   // gridDim.y <= 65535: stride over images
     const long long total = static_cast<long long>(g.VH) * cpr;
     uint64_t acc = 0;
     for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < total;
@@ -335,13 +336,14 @@ __global__ void sse_kernel(const uint8_t* __restrict__ a, const uint8_t* __restr
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    __shared__ uint64_t ws[32];
     if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
     __syncthreads();
     if (threadIdx.x == 0) {
         uint64_t s = 0;
         for (int w = 0; w < (blockDim.x >> 5); ++w) s += ws[w];
         if (s) atomicAdd(sse + n, static_cast<unsigned long long>(s));
+    }
+    __syncthreads();
     }
 }
 
@@ -395,7 +397,7 @@ int launch_psnr(const void* ref, const void* test, const Geom& g, uint64_t* sse,
     const long long chunks = static_cast<long long>(g.VH) * (g.W * g.elem / 16);
     long long gx = (chunks + 255) / 256;
     if (gx > 64) gx = 64;
-    sse_kernel<<<dim3(static_cast<unsigned>(gx), g.N), 256, 0, st>>>(
+    sse_kernel<<<dim3(static_cast<unsigned>(gx), g.N < 65535 ? g.N : 65535), 256, 0, st>>>(
         static_cast<const uint8_t*>(ref), static_cast<const uint8_t*>(test),
         reinterpret_cast<unsigned long long*>(sse), g);
     e = cudaGetLastError();

@@ -558,3 +558,34 @@ def test_pitched_strided_views_every_entry(codec_path):
     rec, _, _ = pkg.codec(t, "zonal", r=16)
     torch.cuda.synchronize()
     assert np.max(np.abs(pkg.ssim(t, rec).cpu().numpy() - oq.ssim(vw, rec.cpu().numpy()))) < 1e-9
+
+
+def test_huge_batch_of_tiny_images():
+    """70,000 images of 16x16 (more than a grid's 65,535 y-dimension): forward,
+    forward16, the fused codec (zonal, uniform), psnr, the sweep and SSIM."""
+    rng = np.random.default_rng(31)
+    imgs = rng.integers(0, 256, size=(70000, 16, 16)).astype(np.uint8)
+    x = to_dev(imgs)
+    Z = oracle_Z(imgs)
+    assert np.array_equal(pkg.forward(x).cpu().numpy(), Z)
+    rec, sse, _ = pkg.codec(x, "zonal", r=16)
+    torch.cuda.synchronize()
+    ref = oc.codec_images(imgs, "zonal", r=16)
+    assert np.array_equal(rec.cpu().numpy(), ref["recon_img"])
+    assert sse.cpu().tolist() == ref["sse"]
+    s2 = torch.empty(70000, dtype=torch.int64, device=DEV)
+    pkg.dct16a_psnr(x, rec, s2)
+    torch.cuda.synchronize()
+    assert s2.cpu().tolist() == ref["sse"]
+    sw, _ = pkg.zonal_sweep(x, 16, 1)
+    torch.cuda.synchronize()
+    assert sw[:, 0].cpu().tolist() == ref["sse"]
+    ss = pkg.ssim(x, rec).cpu().numpy()
+    sel = [0, 65535, 69999]
+    assert np.max(np.abs(ss[sel] - np.array(oq.ssim(imgs[sel], rec.cpu().numpy()[sel])))) < 1e-9
+    f = (imgs.astype(np.int16) * 4)[:20000]
+    fd = to_dev(f)
+    rec, sse, _ = pkg.codec(fd, "uniform", step=16)
+    torch.cuda.synchronize()
+    ref = oc.codec_images(f, "uniform", step=16, bit_depth=10)
+    assert sse.cpu().tolist() == ref["sse"]
