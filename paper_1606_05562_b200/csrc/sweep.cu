@@ -50,7 +50,7 @@ __constant__ ZZTable c_zz = make_zz();
 template <int ELEM>
 struct SCfg {
     static constexpr int kStageBytes = 16 * kWTile * 16 * ELEM;
-    // per warp: stages | Y transposition (2 x 336 floats) | W⊙Z (2 x 256 floats) | SSE[256] u64
+    // per warp: stages | Y transposition (2 x 336 floats) + W⊙Z (2 x 257 floats) | SSE[256] u64
     static constexpr int kYBytes = 3072, kZBytes = 2048, kSseBytes = 2048;
     static constexpr int kWarpBytes = kSStages * kStageBytes + kYBytes + kZBytes + kSseBytes;
     static_assert(kWarpBytes % 1024 == 0, "stages must stay 1024-byte aligned");
@@ -79,8 +79,9 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
     const int h = lane >> 4, t = lane & 15;
     uint8_t* wbase = smem + warp * Cfg::kWarpBytes;
     float* ty = reinterpret_cast<float*>(wbase + kSStages * Cfg::kStageBytes) + h * (16 * 20 + 16);
-    float* wzb = reinterpret_cast<float*>(wbase + kSStages * Cfg::kStageBytes + Cfg::kYBytes);
-    float* wz = wzb + h * 256;
+    // W⊙Z of the block pair right after the Y tile (2 x 336 floats); the second block
+    // starts 257 floats later so the two half-warps' broadcasts hit different banks
+    float* wz = reinterpret_cast<float*>(wbase + kSStages * Cfg::kStageBytes) + 2 * 336 + h * 257;
     unsigned long long* ssew =
         reinterpret_cast<unsigned long long*>(wbase + kSStages * Cfg::kStageBytes + Cfg::kYBytes + Cfg::kZBytes);
     float* Ts = reinterpret_cast<float*>(smem + kSWarps * Cfg::kWarpBytes);   // Ts[k*16 + i] = T[k][i]
@@ -186,51 +187,74 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
             float N[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) N[j] = 1152.5f;
-#pragma unroll 1
-            for (int r = 1; r <= p.r_last; ++r) {
-                const int kl = c_zz.v[r - 1];
-                const int k = kl >> 4, lc = kl & 15;
-                const float sv = wz[kl] * Ts[k * 16 + t];
-                const float4* tr = reinterpret_cast<const float4*>(Ts + lc * 16);
+            // operands of the rank-1 step r (zig-zag cell of rank r-1), prefetched one step ahead
+            float sv;
+            float4 tq[4];
+            auto fetch = [&](int r, float& s_out, float4 (&t_out)[4]) {
+                const int kl = c_zz.v[min(r, 256) - 1];
+                s_out = wz[kl] * Ts[(kl >> 4) * 16 + t];
+                const float4* tr = reinterpret_cast<const float4*>(Ts + (kl & 15) * 16);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) t_out[q] = tr[q];
+            };
+            auto update = [&]() {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const float4 tq = tr[q];
-                    N[4 * q] = fmaf(sv, tq.x, N[4 * q]);
-                    N[4 * q + 1] = fmaf(sv, tq.y, N[4 * q + 1]);
-                    N[4 * q + 2] = fmaf(sv, tq.z, N[4 * q + 2]);
-                    N[4 * q + 3] = fmaf(sv, tq.w, N[4 * q + 3]);
+                    N[4 * q] = fmaf(sv, tq[q].x, N[4 * q]);
+                    N[4 * q + 1] = fmaf(sv, tq[q].y, N[4 * q + 1]);
+                    N[4 * q + 2] = fmaf(sv, tq[q].z, N[4 * q + 2]);
+                    N[4 * q + 3] = fmaf(sv, tq[q].w, N[4 * q + 3]);
                 }
-                if (r >= p.r_first) {
-                    unsigned ei;
-                    if (ELEM == 1) {
-                        // floor((N + 1152.5)/2304) by one round-down FMA onto 2^23 (exact, see
-                        // header); cvt.pack.sat clamps to [0, 255] and packs 4 pixels, then
-                        // vabsdiff4 + dp4a square and sum against the original bytes
-                        ei = 0;
+            };
+            fetch(1, sv, tq);
+#pragma unroll 1
+            for (int r = 1; r < p.r_first; ++r) {   // below the requested range: update only
+                float svn;
+                float4 tqn[4];
+                fetch(r + 1, svn, tqn);
+                update();
+                sv = svn;
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            int v[4];
+                for (int q = 0; q < 4; ++q) tq[q] = tqn[q];
+            }
+#pragma unroll 1
+            for (int r = p.r_first; r <= p.r_last; ++r) {
+                float svn;
+                float4 tqn[4];
+                fetch(r + 1, svn, tqn);
+                update();
+                unsigned ei;
+                if (ELEM == 1) {
+                    // floor((N + 1152.5)/2304) by one round-down FMA onto 2^23 (exact, see
+                    // header); cvt.pack.sat clamps to [0, 255] and packs 4 pixels, then
+                    // vabsdiff4 + dp4a square and sum against the original bytes
+                    ei = 0;
 #pragma unroll
-                            for (int i = 0; i < 4; ++i)
-                                v[i] = static_cast<int>(__float_as_uint(__fmaf_rd(N[4 * q + i], inv2304, 8388608.0f)) -
-                                                        0x4B000000u);
-                            const uint32_t pk = pack2_sat_u8(v[1], v[0], pack2_sat_u8(v[3], v[2], 0u));
-                            const uint32_t d = __vabsdiffu4(pk, xw[q]);
-                            ei = __dp4a(d, d, ei);
-                        }
-                    } else {
-                        float e = 0.0f;
+                    for (int q = 0; q < 4; ++q) {
+                        int v[4];
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const float f = fminf(fmaxf(__fmaf_rd(N[j], inv2304, 8388608.0f), 8388608.0f), top);
-                            const float d = f - xs[j];
-                            e = fmaf(d, d, e);
-                        }
-                        ei = __float2uint_rn(e);
+                        for (int i = 0; i < 4; ++i)
+                            v[i] = static_cast<int>(__float_as_uint(__fmaf_rd(N[4 * q + i], inv2304, 8388608.0f)) -
+                                                    0x4B000000u);
+                        const uint32_t pk = pack2_sat_u8(v[1], v[0], pack2_sat_u8(v[3], v[2], 0u));
+                        const uint32_t d = __vabsdiffu4(pk, xw[q]);
+                        ei = __dp4a(d, d, ei);
                     }
-                    const unsigned tot = __reduce_add_sync(0xffffffffu, contributes ? ei : 0u);
-                    if (lane == 0 && tot) atomicAdd(&ssew[r - p.r_first], static_cast<unsigned long long>(tot));
+                } else {
+                    float e = 0.0f;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const float f = fminf(fmaxf(__fmaf_rd(N[j], inv2304, 8388608.0f), 8388608.0f), top);
+                        const float d = f - xs[j];
+                        e = fmaf(d, d, e);
+                    }
+                    ei = __float2uint_rn(e);
                 }
+                const unsigned tot = __reduce_add_sync(0xffffffffu, contributes ? ei : 0u);
+                if (lane == 0) ssew[r - p.r_first] += tot;   // this warp's own accumulator: no atomic
+                sv = svn;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) tq[q] = tqn[q];
             }
             __syncwarp();
         }
