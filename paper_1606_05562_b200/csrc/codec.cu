@@ -3,7 +3,7 @@
 // PAPER.md:866-910, with S folded into the quantiser.
 // Exactness rules: quant.cuh.
 //
-// Fused codec layout (any r, zonal or uniform, 8- or 10-bit): one warp owns a
+// Generic fused codec layout (zonal, any r, 8- or 10-bit): one warp owns a
 // pair of horizontally adjacent blocks (lanes 0-15: block 2px, lanes 16-31:
 // block 2px+1), one lane per row/column; persistent CTAs walk a contiguous range
 // of block pairs so the per-image SSE is accumulated in registers and flushed
@@ -172,45 +172,27 @@ struct CodecParams {
     int r, step;
 };
 
-template <bool UNIFORM>
-struct CodecCfg {
-    static constexpr int kWarps = UNIFORM ? 4 : 8;   // static smem < 48 KB per CTA
-};
+constexpr int kCodecWarps = 8;   // static smem < 48 KB per CTA
 
-template <bool UNIFORM>
-__global__ void __launch_bounds__(CodecCfg<UNIFORM>::kWarps * 32) codec_kernel(const uint8_t* __restrict__ src, uint8_t* recon,
-                                                                 unsigned long long* sse, const Geom g,
-                                                                 const CodecParams cp) {
-    using V = typename std::conditional<UNIFORM, double, int32_t>::type;
-    constexpr int kCodecWarps = CodecCfg<UNIFORM>::kWarps;
+// Generic fused zonal codec (cross-check kernel, option DCT16A_OPT_CODEC_PATH = 1):
+// exact int32 throughout, N = Tᵀ·(W ⊙ M_r ⊙ Z)·T and pixel = round(N/2304).
+__global__ void __launch_bounds__(kCodecWarps * 32) codec_kernel(const uint8_t* __restrict__ src, uint8_t* recon,
+                                                                unsigned long long* sse, const Geom g,
+                                                                const CodecParams cp) {
     // per warp: forward transposition tile (int32, row pitch 20 words) and
-    // inverse transposition tile (V, row pitch 17); block 1 offset by a bank shift
+    // inverse transposition tile (row pitch 17); block 1 offset by a bank shift
     __shared__ __align__(16) int32_t sy[kCodecWarps][2][16 * 20 + 16];
-    __shared__ V su[kCodecWarps][2][16][17];
+    __shared__ int32_t su[kCodecWarps][2][16][17];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int h = lane >> 4, t = lane & 15;
     int32_t* ty = &sy[warp][h][h * 16];
-    V(*tu)[17] = su[warp][h];
+    int32_t(*tu)[17] = su[warp][h];
 
-    // per-lane constants of column t (lane = column in the column pass)
-    V wcol[16];
-    float ccol[16];
-    uint64_t dcol[16];
+    // per-lane weights of column t (lane = column in the column pass): W ⊙ M_r
+    int32_t wcol[16];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        if constexpr (UNIFORM) {
-            const double s = s_of(k) * s_of(t);
-            wcol[k] = static_cast<double>(cp.step) * s;                        // B̂ = q·Δ·s_k·s_t
-            ccol[k] = static_cast<float>(s / cp.step);                           // 1/(Δ·sqrt(G))
-            dcol[k] = static_cast<uint64_t>(cp.step) * cp.step * (g_of(k) * g_of(t));
-        } else {
-            wcol[k] = zigzag_rank(k, t) < cp.r ? w_of(k, t) : 0;               // W ⊙ M_r
-            ccol[k] = 0.f;
-            dcol[k] = 0;
-        }
-    }
+    for (int k = 0; k < 16; ++k) wcol[k] = zigzag_rank(k, t) < cp.r ? w_of(k, t) : 0;
     const int maxpix = (1 << g.bits) - 1;
-
     const long long p0 = static_cast<long long>(blockIdx.x) * cp.chunk;
     long long p1 = p0 + cp.chunk;
     if (p1 > cp.n_pairs) p1 = cp.n_pairs;
@@ -255,19 +237,16 @@ __global__ void __launch_bounds__(CodecCfg<UNIFORM>::kWarps * 32) codec_kernel(c
 #pragma unroll
             for (int k = 0; k < 16; ++k) col[k] = ty[k * 20 + t];
             net_fwd(col, z);
-            V c[16], u[16];
+            int32_t c[16], u[16];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                if constexpr (UNIFORM) c[k] = static_cast<double>(uniform_level(z[k], ccol[k], dcol[k])) * wcol[k];
-                else c[k] = z[k] * wcol[k];
-            }
+            for (int k = 0; k < 16; ++k) c[k] = z[k] * wcol[k];
             net_inv(c, u);
 #pragma unroll
             for (int i = 0; i < 16; ++i) tu[i][t] = u[i];
         }
         __syncwarp();
         // ---- row t: A′[t, :] = (Tᵀ·B̂)[t, :]·T, round, clamp, SSE, store
-        V rr[16], a[16];
+        int32_t rr[16], a[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) rr[j] = tu[t][j];
         net_inv(rr, a);
@@ -275,8 +254,7 @@ __global__ void __launch_bounds__(CodecCfg<UNIFORM>::kWarps * 32) codec_kernel(c
         uint32_t e = 0;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-            if constexpr (UNIFORM) pix[j] = uniform_pixel(a[j], maxpix);
-            else pix[j] = zonal_pixel(a[j], maxpix);
+            pix[j] = zonal_pixel(a[j], maxpix);
             const int d = pix[j] - x[j];
             e += static_cast<uint32_t>(d * d);
         }
@@ -410,21 +388,16 @@ int launch_codec_generic(const void* src, const Geom& g, const dct16a_quant& q, 
     CodecParams cp;
     cp.PX = (g.BX + 1) / 2;
     cp.n_pairs = static_cast<long long>(g.N) * g.BY * cp.PX;
-    const int warps = q.mode == DCT16A_UNIFORM ? CodecCfg<true>::kWarps : CodecCfg<false>::kWarps;
-    const int ctas_per_sm = 16 / warps;
+    const int ctas_per_sm = 16 / kCodecWarps;
     long long grid = static_cast<long long>(num_sms()) * ctas_per_sm;
-    const long long min_chunk = 4 * warps;
+    const long long min_chunk = 4 * kCodecWarps;
     if (grid * min_chunk > cp.n_pairs) grid = (cp.n_pairs + min_chunk - 1) / min_chunk;
     cp.chunk = (cp.n_pairs + grid - 1) / grid;
     cp.r = q.r;
     cp.step = q.step;
-    auto* s = reinterpret_cast<unsigned long long*>(sse);
-    if (q.mode == DCT16A_UNIFORM)
-        codec_kernel<true><<<static_cast<unsigned>(grid), warps * 32, 0, st>>>(
-            static_cast<const uint8_t*>(src), static_cast<uint8_t*>(recon), s, g, cp);
-    else
-        codec_kernel<false><<<static_cast<unsigned>(grid), warps * 32, 0, st>>>(
-            static_cast<const uint8_t*>(src), static_cast<uint8_t*>(recon), s, g, cp);
+    codec_kernel<<<static_cast<unsigned>(grid), kCodecWarps * 32, 0, st>>>(
+        static_cast<const uint8_t*>(src), static_cast<uint8_t*>(recon), reinterpret_cast<unsigned long long*>(sse), g,
+        cp);
     return static_cast<int>(cudaGetLastError());
 }
 

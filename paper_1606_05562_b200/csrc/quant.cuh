@@ -60,10 +60,5 @@ __device__ __forceinline__ int zonal_pixel(int32_t N, int maxpix) {
     return p > maxpix ? maxpix : p;
 }
 
-__device__ __forceinline__ int uniform_pixel(double a, int maxpix) {
-    if (!(a > 0.0)) return 0;   // round_half_away(a) <= 0 -> clamp 0
-    const double p = floor(a + 0.5);
-    return p > maxpix ? maxpix : static_cast<int>(p);
-}
 
 }  // namespace dct16a
