@@ -137,3 +137,22 @@ def test_forward16_rejects_10bit():
     d = pkg.make_desc(64, 64, 1, 10)
     buf = ctypes.c_void_p(1 << 20)
     assert L.dct16a_forward16(buf, ctypes.byref(d), buf, None) == -5
+
+
+def _build_c_demo():
+    out = os.path.join(ROOT, "build", "c_api_demo")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    pkgdir = os.path.dirname(_lib.LIB_PATH)
+    cuda_lib = "/usr/local/cuda/lib64"
+    cmd = ["gcc", "-O2", "-std=c99", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           os.path.join(ROOT, "examples", "c_api_demo.c"), "-L", pkgdir, "-ldct16a", "-L", cuda_lib, "-lcudart",
+           "-lm", f"-Wl,-rpath,{pkgdir}:{cuda_lib}", "-o", out]
+    return subprocess.run(cmd, capture_output=True, text=True), out
+
+
+def test_c_api_demo_compiles_and_links():
+    """The ABI is usable from plain C: the demo compiles against include/dct16a.h
+    and links against libdct16a.so (tests/test_gpu_parity.py runs it)."""
+    r, out = _build_c_demo()
+    assert r.returncode == 0, r.stderr
+    assert os.path.exists(out)

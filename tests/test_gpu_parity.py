@@ -589,3 +589,13 @@ def test_huge_batch_of_tiny_images():
     torch.cuda.synchronize()
     ref = oc.codec_images(f, "uniform", step=16, bit_depth=10)
     assert sse.cpu().tolist() == ref["sse"]
+
+
+def test_c_api_demo_runs():
+    import subprocess
+    import test_abi
+    r, out = test_abi._build_c_demo()
+    assert r.returncode == 0, r.stderr
+    run = subprocess.run([out], capture_output=True, text=True, timeout=120)
+    assert run.returncode == 0, run.stdout + run.stderr
+    assert "c_api_demo ok" in run.stdout
