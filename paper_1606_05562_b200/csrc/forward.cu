@@ -392,11 +392,12 @@ int launch_fwd_t(const void* src, const Geom& g, int32_t* coef, cudaStream_t st)
 
 // Output path of the forward kernel.  Default (8-bit): one 32 KB TMA tensor
 // store of the whole tile (mode 5), measured fastest on config 2 with the
-// dynamic tile scheduler (6.72 TB/s); the option DCT16A_OPT_FWD_STORE (include/dct16a.h) selects
+// dynamic tile scheduler (6.72 TB/s); 10-bit: 8 KB stores
+// (mode 3, 6.68 TB/s on 200 config-4 frames, tools/fwd10_modes.py); the option DCT16A_OPT_FWD_STORE (include/dct16a.h) selects
 // the other variants for experiments (profiles/r01_fwd_store_modes.md).
 int store_mode(int elem) {
     const int m = get_option(DCT16A_OPT_FWD_STORE);
-    return m >= 0 ? m : (elem == 1 ? 5 : 0);
+    return m >= 0 ? m : (elem == 1 ? 5 : 3);
 }
 
 template <int ELEM>
