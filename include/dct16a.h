@@ -161,6 +161,27 @@ DCT16A_API int dct16a_codec(const void* src, const dct16a_desc* desc,
                             uint64_t* sse, double* psnr, void* stream);
 
 /*
+ * dct16a_codec_allreduce — dct16a_codec with the path's only exchange fused
+ * into the kernel (config 4 across GPUs):
+ * instead of a local SSE vector and a separate all-reduce, every image's SSE
+ * is added with system-scope 64-bit atomics into sse_peers[q][frame_offset + n]
+ * for every q < n_peers — the per-frame SSE vectors of all ranks, mapped into
+ * this device's address space (e.g. torch symmetric memory buffer_ptrs over
+ * NVLink).  Integer adds: every rank ends with the exact sums, independent of
+ * order.  The caller zeroes every rank's vector and synchronises the ranks
+ * before the call, and again after every rank's kernel has completed, before
+ * reading; PSNR follows from the summed vector.
+ *   sse_peers   : HOST array of n_peers device pointers (each 8-byte aligned).
+ *   n_peers     : 1..8.
+ *   frame_offset: index of this call's first image in the global vector.
+ * Runs the warp-per-block-pair kernel for every mode.  Errors as dct16a_codec;
+ * DCT16A_EDOMAIN for n_peers outside [1, 8] or frame_offset < 0.
+ */
+DCT16A_API int dct16a_codec_allreduce(const void* src, const dct16a_desc* desc, const dct16a_quant* quant,
+                                      void* recon, uint64_t* const* sse_peers, int32_t n_peers,
+                                      int64_t frame_offset, void* stream);
+
+/*
  * dct16a_ssim — mean SSIM per image (Wang et al. 2004):
  * 11x11 Gaussian window (sigma 1.5, unit sum), K1 = 0.01, K2 = 0.03,
  * L = 2^b - 1, full resolution, averaged over every window position that lies

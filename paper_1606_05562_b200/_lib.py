@@ -59,6 +59,8 @@ def lib() -> ctypes.CDLL:
         L.dct16a_codec.argtypes = [vp, P(Desc), P(Quant), vp, vp, vp, vp]
         for f in ("dct16a_forward", "dct16a_quantize", "dct16a_inverse", "dct16a_psnr", "dct16a_codec"):
             getattr(L, f).restype = ctypes.c_int
+        L.dct16a_codec_allreduce.argtypes = [vp, P(Desc), P(Quant), vp, P(vp), ctypes.c_int32, ctypes.c_int64, vp]
+        L.dct16a_codec_allreduce.restype = ctypes.c_int
         L.dct16a_forward16.argtypes = [vp, P(Desc), vp, vp]
         L.dct16a_forward16.restype = ctypes.c_int
         L.dct16a_ssim.argtypes = [vp, vp, P(Desc), vp, vp]
@@ -149,6 +151,16 @@ def dct16a_codec(src, quant: Quant, sse, recon=None, psnr=None, desc: Desc | Non
     d = desc if desc is not None else desc_of(src)
     _check(lib().dct16a_codec(_ptr(src), ctypes.byref(d), ctypes.byref(quant), _ptr(recon), _ptr(sse),
                               _ptr(psnr), _stream(stream)))
+
+
+def dct16a_codec_allreduce(src, quant: Quant, sse_peers, frame_offset: int, recon=None, desc: Desc | None = None,
+                           stream=None) -> None:
+    """sse_peers: sequence of device addresses (ints) of every rank's int64 SSE
+    vector, mapped into this device (e.g. torch symmetric memory buffer_ptrs)."""
+    d = desc if desc is not None else desc_of(src)
+    arr = (ctypes.c_void_p * len(sse_peers))(*[ctypes.c_void_p(int(a)) for a in sse_peers])
+    _check(lib().dct16a_codec_allreduce(_ptr(src), ctypes.byref(d), ctypes.byref(quant), _ptr(recon), arr,
+                                        len(sse_peers), int(frame_offset), _stream(stream)))
 
 
 def dct16a_forward16(src, coef16, desc: Desc | None = None, stream=None) -> None:

@@ -226,6 +226,27 @@ DCT16A_API int dct16a_codec(const void* src, const dct16a_desc* desc, const dct1
                     "dct16a_codec");
 }
 
+DCT16A_API int dct16a_codec_allreduce(const void* src, const dct16a_desc* desc, const dct16a_quant* quant,
+                                      void* recon, uint64_t* const* sse_peers, int32_t n_peers, int64_t frame_offset,
+                                      void* stream) {
+    Geom g;
+    int rc;
+    if ((rc = check_desc(desc, &g)) || (rc = check_quant(quant))) return rc;
+    if ((rc = check_ptr(src, "src"))) return rc;
+    if (recon && !aligned16(recon)) return fail(DCT16A_EALIGN, "recon is not 16-byte aligned");
+    if (recon == src) return fail(DCT16A_EDOMAIN, "recon must not alias src");
+    if (!sse_peers) return fail(DCT16A_ENULL, "sse_peers is NULL");
+    if (n_peers < 1 || n_peers > 8) return fail(DCT16A_EDOMAIN, "n_peers %d outside [1, 8]", n_peers);
+    if (frame_offset < 0) return fail(DCT16A_EDOMAIN, "frame_offset %lld < 0", static_cast<long long>(frame_offset));
+    for (int i = 0; i < n_peers; ++i) {
+        if (!sse_peers[i]) return fail(DCT16A_ENULL, "sse_peers[%d] is NULL", i);
+        if (reinterpret_cast<uintptr_t>(sse_peers[i]) & 7u) return fail(DCT16A_EALIGN, "sse_peers[%d] not 8-byte aligned", i);
+    }
+    return launched(launch_codec_allreduce(src, g, *quant, recon, sse_peers, n_peers, frame_offset,
+                                           static_cast<cudaStream_t>(stream)),
+                    "dct16a_codec_allreduce");
+}
+
 DCT16A_API int dct16a_ssim(const void* ref, const void* test, const dct16a_desc* desc, double* ssim,
                            void* stream) {
     Geom g;

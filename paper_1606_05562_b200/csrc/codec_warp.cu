@@ -69,10 +69,17 @@ struct WCfg {
     static constexpr int kCtasPerSm = UNIFORM ? (kFit < DCT16A_CW_UCTAS ? kFit : DCT16A_CW_UCTAS) : (kFit < 4 ? kFit : 4);
 };
 
+constexpr int kMaxPeers = 8;
+
 struct WParams {
     int W, BX, BY, VH, tiles_per_strip, maxpix;
     long long n_tiles, chunk;
     int has_recon;
+    // fused SSE all-reduce (dct16a_codec_allreduce): every image's SSE is added
+    // into sse_peers[q][frame_offset + n] of every peer q; n_peers = 0: local sse
+    int n_peers;
+    long long frame_offset;
+    unsigned long long* peers[kMaxPeers];
     // zonal
     int r;
     // uniform
@@ -137,6 +144,17 @@ __device__ __noinline__ int32_t uniform_fix_call(float z, int32_t m, int step, i
 }
 
 }  // namespace
+
+// Add one image's SSE: locally, or into every peer's vector over NVLink (system-
+// scope 64-bit atomics on peer-mapped memory: integer adds, order-independent,
+// so every rank ends with the exact per-frame sums — the path's all-reduce).
+__device__ __forceinline__ void flush_sse(unsigned long long* sse, const WParams& p, int n, unsigned long long v) {
+    if (p.n_peers == 0) {
+        atomicAdd(sse + n, v);
+        return;
+    }
+    for (int q = 0; q < p.n_peers; ++q) atomicAdd_system(p.peers[q] + p.frame_offset + n, v);
+}
 
 template <int ELEM, bool UNIFORM>
 __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
@@ -217,7 +235,7 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
         if (n != cur_n) {
 #pragma unroll
             for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0 && acc) atomicAdd(sse + cur_n, acc);
+            if (lane == 0 && acc) flush_sse(sse, p, cur_n, acc);
             acc = 0;
             cur_n = n;
         }
@@ -380,7 +398,7 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
-        if (acc) atomicAdd(sse + cur_n, acc);
+        if (acc) flush_sse(sse, p, cur_n, acc);
         if (p.has_recon) bulk_wait<0>();
     }
 }
@@ -388,7 +406,8 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
 namespace {
 
 template <int ELEM, bool UNIFORM>
-int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse, cudaStream_t st) {
+int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse, cudaStream_t st,
+              uint64_t* const* peers = nullptr, int n_peers = 0, long long frame_offset = 0) {
     using Cfg = WCfg<ELEM, UNIFORM>;
     CUtensorMap tin, tout;
     const uint64_t dims[3] = {uint64_t(g.W), uint64_t(g.H), uint64_t(g.N)};
@@ -414,6 +433,9 @@ int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon
     p.maxpix = (1 << g.bits) - 1;
     p.n_tiles = static_cast<long long>(g.N) * g.BY * p.tiles_per_strip;
     p.has_recon = recon != nullptr;
+    p.n_peers = n_peers;
+    p.frame_offset = frame_offset;
+    for (int i = 0; i < n_peers; ++i) p.peers[i] = reinterpret_cast<unsigned long long*>(peers[i]);
     p.r = q.r;
     p.step = q.step;
     if (UNIFORM) {
@@ -462,6 +484,16 @@ int launch_codec_warp(const void* src, const Geom& g, const dct16a_quant& q, voi
     const bool uni = q.mode == DCT16A_UNIFORM;
     if (g.elem == 1) return uni ? launch_cw<1, true>(src, g, q, recon, sse, st) : launch_cw<1, false>(src, g, q, recon, sse, st);
     return uni ? launch_cw<2, true>(src, g, q, recon, sse, st) : launch_cw<2, false>(src, g, q, recon, sse, st);
+}
+
+int launch_codec_allreduce(const void* src, const Geom& g, const dct16a_quant& q, void* recon,
+                           uint64_t* const* peers, int n_peers, long long frame_offset, cudaStream_t st) {
+    const bool uni = q.mode == DCT16A_UNIFORM;
+    if (g.elem == 1)
+        return uni ? launch_cw<1, true>(src, g, q, recon, nullptr, st, peers, n_peers, frame_offset)
+                   : launch_cw<1, false>(src, g, q, recon, nullptr, st, peers, n_peers, frame_offset);
+    return uni ? launch_cw<2, true>(src, g, q, recon, nullptr, st, peers, n_peers, frame_offset)
+               : launch_cw<2, false>(src, g, q, recon, nullptr, st, peers, n_peers, frame_offset);
 }
 
 }  // namespace dct16a

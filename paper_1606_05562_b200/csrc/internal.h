@@ -50,6 +50,9 @@ int launch_ssim(const void* ref, const void* test, const Geom& g, double* ssim, 
 int launch_sweep(const void* src, const Geom& g, int r_first, int r_count, uint64_t* sse, double* psnr,
                  cudaStream_t st);
 int launch_psnr_finish(const Geom& g, long long count, uint64_t* sse, double* psnr, cudaStream_t st);
+// fused codec + SSE all-reduce over peer memory (codec_warp.cu)
+int launch_codec_allreduce(const void* src, const Geom& g, const dct16a_quant& q, void* recon,
+                           uint64_t* const* peers, int n_peers, long long frame_offset, cudaStream_t st);
 // library options (dct16a_set_option); read by the launchers
 int get_option(int option);
 

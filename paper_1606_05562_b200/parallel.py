@@ -34,6 +34,35 @@ def reduce_sse(local_sse, offset: int, n_total: int, group=None):
     return full
 
 
+class FusedSseAllReduce:
+    """The config-4 exchange fused into the codec kernel (dct16a_codec_allreduce):
+    one int64 [n_total] SSE vector per rank in torch symmetric memory; every
+    rank's kernel adds each local frame's SSE into all ranks' vectors over
+    peer-mapped memory (NVLink).  Symmetric-memory barriers order the zeroing
+    before, and the reads after, every rank's kernel.  Reuse one instance."""
+
+    def __init__(self, n_total: int, device, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.n_total = n_total
+        self.buf = symm.empty(n_total, dtype=torch.int64, device=device)
+        self.handle = symm.rendezvous(self.buf, group if group is not None else dist.group.WORLD)
+        self.peers = list(self.handle.buffer_ptrs)
+        if len(self.peers) > 8:
+            raise ValueError("dct16a_codec_allreduce supports up to 8 peers")
+
+    def run(self, frames, quant, frame_offset: int, recon=None, desc=None, stream=None):
+        """Codec of this rank's frames; returns the all-reduced per-frame SSE (int64)."""
+        from . import _lib
+        self.buf.zero_()
+        self.handle.barrier()            # every rank's vector is zero before any kernel adds
+        if frames is not None and frames.shape[0] > 0:
+            _lib.dct16a_codec_allreduce(frames, quant, self.peers, frame_offset, recon, desc, stream)
+        self.handle.barrier()            # every rank's kernel has finished adding
+        return self.buf
+
+
 def psnr_from_sse(sse_total: int, n_pixels: int, bit_depth: int) -> float:
     """10·log10(peak²·P/SSE), +inf for SSE = 0 (reading A7)."""
     if sse_total == 0:

@@ -23,7 +23,7 @@ def declared_symbols():
 def test_library_loads_and_exports_header_symbols():
     L = pkg.lib()
     syms = declared_symbols()
-    assert len(syms) == 12
+    assert len(syms) == 13
     for s in syms:
         assert hasattr(L, s), s
     out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
@@ -156,3 +156,18 @@ def test_c_api_demo_compiles_and_links():
     r, out = _build_c_demo()
     assert r.returncode == 0, r.stderr
     assert os.path.exists(out)
+
+
+def test_codec_allreduce_validation():
+    L = pkg.lib()
+    d = pkg.make_desc(64, 64, 1, 8)
+    q = pkg.make_quant("uniform", step=16)
+    buf = ctypes.c_void_p(1 << 20)
+    peers = (ctypes.c_void_p * 2)(ctypes.c_void_p(1 << 20), ctypes.c_void_p(2 << 20))
+    f = L.dct16a_codec_allreduce
+    assert f(buf, ctypes.byref(d), ctypes.byref(q), None, peers, 0, 0, None) == -5
+    assert f(buf, ctypes.byref(d), ctypes.byref(q), None, peers, 9, 0, None) == -5
+    assert f(buf, ctypes.byref(d), ctypes.byref(q), None, peers, 2, -1, None) == -5
+    assert f(buf, ctypes.byref(d), ctypes.byref(q), None, None, 2, 0, None) == -1
+    bad = (ctypes.c_void_p * 1)(ctypes.c_void_p((1 << 20) + 4))
+    assert f(buf, ctypes.byref(d), ctypes.byref(q), None, bad, 1, 0, None) == -4

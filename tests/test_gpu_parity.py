@@ -464,13 +464,15 @@ def test_config4_sharded_runner_torchrun():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(root, "tools", "run_config4.py"),
-           "--frames", "5", "--height", "64", "--width", "208", "--reps", "1", "--dump"]
+           "--frames", "5", "--height", "64", "--width", "208", "--reps", "1", "--dump", "--fused"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     f = synth.frames_10bit(range(5), H=64, W=208, workers=1)
     ref = oc.codec_images(f, "uniform", step=16, bit_depth=10)
     assert line["sse"] == ref["sse"]
+    # the in-kernel all-reduce over symmetric memory (dct16a_codec_allreduce) agrees
+    assert line["fused_allreduce"]["equal_to_nccl"] is True
     P = 5 * 64 * 208
     assert abs(line["global_psnr_db"] - oc.psnr_from_sse(sum(ref["sse"]), P, 10)) < 1e-9
 

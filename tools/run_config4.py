@@ -35,6 +35,9 @@ def main():
     ap.add_argument("--step", type=int, default=16)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--dump", action="store_true", help="print the per-frame SSE vector")
+    ap.add_argument("--fused", action="store_true",
+                    help="fuse the SSE all-reduce into the kernel (dct16a_codec_allreduce over symmetric memory) "
+                         "and check it against the NCCL path")
     a = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -42,8 +45,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if world > 1 or a.fused:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29561")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
 
     f0, f1 = parallel.shard(a.frames, world, rank)
     x = torch.from_numpy(synth.frames_10bit(range(f0, f1), H=a.height, W=a.width, total=1000)).to(dev)
@@ -76,6 +81,18 @@ def main():
     r1.record(stream)
     r1.synchronize()
     ar_ms = torch.tensor([r0.elapsed_time(r1)], dtype=torch.float64, device=dev)
+    fused = None
+    if a.fused:
+        fz = parallel.FusedSseAllReduce(a.frames, dev)
+        got = fz.run(x if n else None, q, f0, None, d, stream)
+        torch.cuda.synchronize()
+        f_e0, f_e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f_e0.record(stream)
+        for _ in range(a.reps):
+            got = fz.run(x if n else None, q, f0, None, d, stream)
+        f_e1.record(stream)
+        f_e1.synchronize()
+        fused = {"ms": f_e0.elapsed_time(f_e1) / a.reps, "equal_to_nccl": bool(torch.equal(got, full))}
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         dist.all_reduce(ar_ms, op=dist.ReduceOp.MAX)
@@ -87,10 +104,12 @@ def main():
                 "codec_ms_max_over_ranks": float(ms.item()), "allreduce_ms": float(ar_ms.item()),
                 "blocks_per_s": blocks / (float(ms.item()) / 1e3),
                 "global_psnr_db": parallel.psnr_from_sse(tot, P, 10), "sse_total": tot}
+        if fused is not None:
+            line["fused_allreduce"] = fused
         if a.dump:
             line["sse"] = full.cpu().tolist()
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
