@@ -144,6 +144,26 @@ int get_option(int option) {
     return 0;
 }
 
+int smem_optin(const void* func, int bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static std::mutex mu;
+    static struct Entry {
+        const void* f;
+        uint64_t devmask;
+    } done[64];
+    static int n_done = 0;
+    std::lock_guard<std::mutex> lock(mu);
+    int i = 0;
+    while (i < n_done && done[i].f != func) ++i;
+    if (i < n_done && dev < 64 && ((done[i].devmask >> dev) & 1u)) return 0;
+    const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e) return static_cast<int>(e);
+    if (i == n_done && n_done < 64) done[n_done++] = {func, 0};
+    if (i < n_done && dev < 64) done[i].devmask |= uint64_t(1) << dev;
+    return 0;
+}
+
 int num_sms() {
     int dev = 0;
     cudaGetDevice(&dev);

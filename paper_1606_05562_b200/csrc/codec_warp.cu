@@ -463,11 +463,7 @@ int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon
         // the same word from bits >> F = (magic_bits >> F) + m (arithmetic mod 2^32)
         p.hi_c2 = static_cast<int>(static_cast<uint32_t>(p.hi_c) - ((p.magic_bits >> p.F) << p.hi_shift));
     }
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(codec_warp_kernel<ELEM, UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
-        attr = true;
-    }
+    if (int e = smem_optin(reinterpret_cast<const void*>(codec_warp_kernel<ELEM, UNIFORM>), Cfg::kSmem)) return e;
     long long warps = static_cast<long long>(num_sms()) * Cfg::kCtasPerSm * kWWarps;
     if (warps > p.n_tiles) warps = p.n_tiles;
     p.chunk = (p.n_tiles + warps - 1) / warps;

@@ -375,11 +375,7 @@ int launch_fwd_t(const void* src, const Geom& g, int32_t* coef, cudaStream_t st)
     p.box_w = box_w;
     p.n_tiles = static_cast<long long>(g.N) * g.BY * p.tiles_per_strip;
 
-    static bool attr_set = false;   // idempotent; benign race
-    if (!attr_set) {
-        cudaFuncSetAttribute(fwd_kernel<ELEM, SM>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
-        attr_set = true;
-    }
+    if (int e = smem_optin(reinterpret_cast<const void*>(fwd_kernel<ELEM, SM>), Cfg::kSmem)) return e;
     const long long want = (p.n_tiles + Cfg::kWarps - 1) / Cfg::kWarps;
     long long grid = static_cast<long long>(num_sms()) * Cfg::kMinCtas;
     if (want < grid) grid = want;

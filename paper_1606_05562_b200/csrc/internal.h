@@ -26,6 +26,11 @@ int encode_tiled(CUtensorMap* map, CUtensorMapDataType dt, uint32_t rank, const 
 
 int num_sms();
 
+// Opt a kernel into `bytes` of dynamic shared memory on the current device, once
+// per (kernel, device): the attribute is per device, so a process driving
+// several GPUs must set it on each.  Returns a cudaError_t.
+int smem_optin(const void* func, int bytes);
+
 // Launchers: return cudaError_t of the launch (cudaSuccess = 0) or a negative
 // DCT16A_E* code for encode failures.
 int launch_forward(const void* src, const Geom& g, int32_t* coef, cudaStream_t st);

@@ -294,11 +294,7 @@ int launch_sweep_t(const void* src, const Geom& g, int r_first, int r_count, uin
     p.r_first = r_first;
     p.r_count = r_count;
     p.r_last = r_first + r_count - 1;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(sweep_kernel<ELEM>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
-        attr = true;
-    }
+    if (int e = smem_optin(reinterpret_cast<const void*>(sweep_kernel<ELEM>), Cfg::kSmem)) return e;
     long long warps = static_cast<long long>(num_sms()) * Cfg::kCtasPerSm * kSWarps;
     if (warps > p.n_tiles) warps = p.n_tiles;
     p.chunk = (p.n_tiles + warps - 1) / warps;

@@ -275,11 +275,7 @@ int launch_ztpb(const void* src, const Geom& g, int r, void* recon, uint64_t* ss
     if (warps > p.n_tiles) warps = p.n_tiles;
     p.chunk = (p.n_tiles + warps - 1) / warps;
     const long long grid = (warps + kZWarps - 1) / kZWarps;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(zonal_tpb_kernel<BAND>, cudaFuncAttributeMaxDynamicSharedMemorySize, kZSmem);
-        attr = true;
-    }
+    if (int e = smem_optin(reinterpret_cast<const void*>(zonal_tpb_kernel<BAND>), kZSmem)) return e;
     zonal_tpb_kernel<BAND><<<static_cast<unsigned>(grid), kZWarps * 32, kZSmem, st>>>(
         tin, tout, reinterpret_cast<unsigned long long*>(sse), p);
     return static_cast<int>(cudaGetLastError());
