@@ -31,7 +31,13 @@ namespace dct16a {
 namespace {
 
 constexpr int kZTile = 32;
-constexpr int kZStages = 3;
+#ifndef DCT16A_ZTPB_STAGES
+#define DCT16A_ZTPB_STAGES 3
+#endif
+#ifndef DCT16A_ZTPB_CTAS
+#define DCT16A_ZTPB_CTAS 2
+#endif
+constexpr int kZStages = DCT16A_ZTPB_STAGES;
 constexpr int kZWarps = 4;
 constexpr int kZStageBytes = 16 * 512;   // 16 rows x 512 u8 pixels
 constexpr int kZSmem = 1024 + kZWarps * (kZStages * kZStageBytes + kZStages * 8);
@@ -76,7 +82,7 @@ __device__ __forceinline__ void z_store(const CUtensorMap* tout, const ZParams& 
 }  // namespace
 
 template <int BAND>
-__global__ void __launch_bounds__(kZWarps * 32, 2)
+__global__ void __launch_bounds__(kZWarps * 32, DCT16A_ZTPB_CTAS)
     zonal_tpb_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
                      unsigned long long* __restrict__ sse, const ZParams p) {
     extern __shared__ uint8_t smem_raw[];
@@ -271,7 +277,7 @@ int launch_ztpb(const void* src, const Geom& g, int r, void* recon, uint64_t* ss
     p.n_tiles = static_cast<long long>(g.N) * g.BY * p.tiles_per_strip;
     p.r = r;
     p.has_recon = recon != nullptr;
-    long long warps = static_cast<long long>(num_sms()) * 2 * kZWarps;
+    long long warps = static_cast<long long>(num_sms()) * DCT16A_ZTPB_CTAS * kZWarps;
     if (warps > p.n_tiles) warps = p.n_tiles;
     p.chunk = (p.n_tiles + warps - 1) / warps;
     const long long grid = (warps + kZWarps - 1) / kZWarps;
