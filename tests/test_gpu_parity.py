@@ -601,3 +601,19 @@ def test_c_api_demo_runs():
     run = subprocess.run([out], capture_output=True, text=True, timeout=120)
     assert run.returncode == 0, run.stdout + run.stderr
     assert "c_api_demo ok" in run.stdout
+
+
+@pytest.mark.parametrize("mode", range(8))
+def test_forward_every_store_mode(mode):
+    """Every K1 output path (DCT16A_OPT_FWD_STORE 0..7) is bit-exact, 8- and
+    10-bit, ragged strips and narrow images."""
+    old = pkg.dct16a_get_option(pkg.OPT_FWD_STORE)
+    pkg.dct16a_set_option(pkg.OPT_FWD_STORE, mode)
+    try:
+        for name, imgs in u8_cases():
+            if name in ("cfg1", "ragged17x3", "wide", "tiny", "narrow"):
+                assert np.array_equal(gpu_Z(to_dev(imgs)), oracle_Z(imgs)), name
+        f = synth.frames_10bit([0, 1], H=64, W=272, workers=1)
+        assert np.array_equal(gpu_Z(to_dev(f)), oracle_Z(f))
+    finally:
+        pkg.dct16a_set_option(pkg.OPT_FWD_STORE, old)
