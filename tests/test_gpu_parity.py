@@ -617,3 +617,18 @@ def test_forward_every_store_mode(mode):
         assert np.array_equal(gpu_Z(to_dev(f)), oracle_Z(f))
     finally:
         pkg.dct16a_set_option(pkg.OPT_FWD_STORE, old)
+
+
+@pytest.mark.parametrize("step", [8, 24, 40, 72])
+def test_codec_uniform_reconstruction_ties(step, codec_path):
+    """Flat blocks: only the DC level survives, A′ = Δ·q00/16, an exact .5 tie
+    whenever Δ·q00 ≡ 8 (mod 16) — the fused kernel must send those pixels to
+    the exact decision (round half away from zero)."""
+    v = np.arange(256, dtype=np.uint8).reshape(16, 16)
+    imgs = np.kron(v, np.ones((16, 16), dtype=np.uint8))[None]          # 256 flat blocks, values 0..255
+    _codec_check(imgs, "uniform", 8, step=step)
+    f = (np.kron(np.arange(256).reshape(16, 16) * 4 + 1, np.ones((16, 16), dtype=np.int64))).astype(np.int16)[None]
+    _codec_check(f, "uniform", 10, step=step)
+    ref = oc.codec_images(imgs, "uniform", step=step, bit_depth=8)
+    if step in (24, 40, 72):
+        assert ref["n_near_ties"] > 0
