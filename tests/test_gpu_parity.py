@@ -632,3 +632,60 @@ def test_codec_uniform_reconstruction_ties(step, codec_path):
     ref = oc.codec_images(imgs, "uniform", step=step, bit_depth=8)
     if step in (24, 40, 72):
         assert ref["n_near_ties"] > 0
+
+
+def _random_case(rng):
+    bd = int(rng.choice([8, 10]))
+    elem = 1 if bd == 8 else 2
+    H = 16 * int(rng.integers(1, 9))
+    W = 16 * int(rng.integers(1, 26))
+    n = int(rng.integers(1, 4))
+    pad_w = 16 * int(rng.integers(0, 3)) // elem          # extra pixels per row (pitch > width)
+    pad_h = int(rng.integers(0, 3))                      # extra rows per image (stride > pitch·height)
+    hi = 256 if bd == 8 else 1024
+    base = rng.integers(0, hi, size=(n, H + pad_h, W + pad_w)).astype(np.uint8 if bd == 8 else np.int16)
+    smooth = rng.random() < 0.5
+    if smooth:   # AR(1)-like smooth content so that quantisation keeps structure
+        field = np.cumsum(np.cumsum(rng.normal(size=base.shape), axis=1), axis=2)
+        field = (field - field.min()) / max(1e-9, np.ptp(field)) * (hi - 1)
+        base = np.rint(field).astype(base.dtype)
+    return bd, base
+
+
+@pytest.mark.parametrize("seed", range(32))
+def test_random_shapes_every_entry(seed):
+    """Seeded random geometries (widths 16..400, heights 16..128, pitched and
+    strided windows, batches 1-3, 8/10-bit, random r and Δ): forward, the fused
+    codec on every kernel, the r-sweep and SSIM against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    bd, base = _random_case(rng)
+    n, Hp, Wp = base.shape
+    H = max(16, (Hp // 16) * 16)
+    W = max(16, (Wp // 16) * 16)
+    view = base[:, :H, :W]
+    vc = np.ascontiguousarray(view)
+    t = to_dev(base)[:, :H, :W]
+    assert np.array_equal(gpu_Z(t), oracle_Z(vc))
+    r = int(rng.integers(1, 257))
+    step = int(rng.integers(1, 100))
+    old = pkg.dct16a_get_option(pkg.OPT_CODEC_PATH)
+    try:
+        for path in (0, 1, 2):
+            pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, path)
+            for mode in ("zonal", "uniform"):
+                rec, sse, _ = pkg.codec(t, mode, r=r, step=step)
+                torch.cuda.synchronize()
+                ref = oc.codec_images(vc, mode, r=r, step=step, bit_depth=bd)
+                assert np.array_equal(rec.cpu().numpy(), ref["recon_img"]), (path, mode, r, step)
+                assert sse.cpu().tolist() == ref["sse"], (path, mode)
+    finally:
+        pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, old)
+    r0 = int(rng.integers(1, 250))
+    s, _ = pkg.zonal_sweep(t, r0, 3)
+    torch.cuda.synchronize()
+    for i in range(3):
+        assert s[:, i].cpu().tolist() == oc.codec_images(vc, "zonal", r=r0 + i, bit_depth=bd)["sse"]
+    rec, _, _ = pkg.codec(t, "zonal", r=r)
+    torch.cuda.synchronize()
+    got = pkg.ssim(t, rec).cpu().numpy()
+    assert np.max(np.abs(got - np.array(oq.ssim(vc, rec.cpu().numpy(), bd)))) < 1e-9
