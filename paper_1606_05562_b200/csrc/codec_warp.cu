@@ -342,12 +342,15 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
                         for (int j = 0; j < 16; ++j) pix[j] = fix[j];
                     }
                 } else {
+                    // floor((N + 1152.5)/2304) by one round-down FMA onto 2^23 (exact: the
+                    // product errs by < 2^-24·t, below the 1/4608 distance of an odd
+                    // multiple of 1/4608 to an integer for t < 3640); 8-bit clamps in the
+                    // saturating pack below, 10-bit here
                     const float inv2304 = 1.0f / 2304.0f;
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
-                        const float tt = fmaxf(a[j] * inv2304, 0.0f);
-                        const uint32_t bits = min(__float_as_uint(__fadd_rd(tt, 8388608.0f)), 0x4B000000u + p.maxpix);
-                        pix[j] = static_cast<int>(bits - 0x4B000000u);
+                        const int v = static_cast<int>(__float_as_uint(__fmaf_rd(a[j], inv2304, 8388608.0f)) - 0x4B000000u);
+                        pix[j] = ELEM == 1 ? v : __vimin_s32_relu(v, p.maxpix);
                     }
                 }
             }
@@ -360,8 +363,8 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
                 if (ELEM == 1) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        o[q] = __byte_perm(__byte_perm(pix[4 * q], pix[4 * q + 1], 0x0040),
-                                           __byte_perm(pix[4 * q + 2], pix[4 * q + 3], 0x0040), 0x5410);
+                        // clamp to [0, 255] and pack four pixels (cvt.pack.sat)
+                        o[q] = pack2_sat_u8(pix[4 * q + 1], pix[4 * q], pack2_sat_u8(pix[4 * q + 3], pix[4 * q + 2], 0u));
                         const uint32_t d = __vabsdiffu4(o[q], w[q]);
                         e = __dp4a(d, d, e);
                     }
