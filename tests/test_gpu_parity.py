@@ -444,6 +444,12 @@ def test_config5_full_size_sampled():
     torch.cuda.synchronize()
     got = sse.cpu().numpy()
     assert np.all(got[:, 255] == 0)
+    # SSIM of the r = 16 reconstructions (the paper's second measure)
+    rec, _, _ = pkg.codec(x, "zonal", r=16)
+    ss = pkg.ssim(x, rec).cpu().numpy()
+    recn = rec.cpu().numpy()
+    for n in (0, 16, 32, 48):
+        assert abs(ss[n] - oq.ssim(imgs[n:n + 1], recn[n:n + 1])[0]) < 1e-9
     for n in (0, 16, 32, 48):
         img = imgs[n:n + 1]
         X = oc.to_blocks(img.astype(np.int64))
