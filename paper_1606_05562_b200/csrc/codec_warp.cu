@@ -20,13 +20,21 @@
 //   value whose fraction falls in the window [0, δ + 2·err) is re-decided
 //   exactly in integers (uniform_fix).
 // * Uniform inverse in float64 (reading A10): the level enters as the double
-//   1.5·2^E + m built from its bits, and one DFMA with the signed weight
-//   Δ·s_k·s_l and the constant −fl(1.5·2^E·w) forms the input (error < 1e-11);
-//   two 60-add networks, smem transposition in between; rounding by one
-//   round-down add (round_f64), pixels within 2^-20 of a .5 boundary are
-//   decided exactly (uniform_exact_floor).
+//   1.5·2^E + m whose high word is one IMAD of the float's bits; one DFMA with
+//   the weight Δ·s_k·s_l and the constant −fl(1.5·2^E·w) forms the input
+//   (error < 1e-11) and the sign of Z flips the result's sign bit; two 60-add
+//   networks, smem transposition in between; rounding by one round-down add
+//   onto 1.5·2^20 + 1/2 (high word = pixel, low word = fraction), clamp by one
+//   relu-min; a pixel within 2^-20 of a .5 boundary sends the warp to the exact
+//   decision (exact_row_fix → uniform_exact_floor).
 // * Zonal inverse in float32, exact (half-integers < 2^23): N + 1152.5 on the
-//   DC input, pixel = floor((N + 1152.5)/2304) as in zonal_tpb.cu.
+//   DC input, pixel = floor((N + 1152.5)/2304) by one round-down FMA; 8-bit
+//   pixels are clamped and packed by cvt.pack.sat.
+// * SSE: per row, vabsdiff4/dp4a (8-bit) or integer squares (10-bit), one
+//   64-bit atomic per warp and image (or, for dct16a_codec_allreduce, into
+//   every rank's vector over peer memory).
+// * Schedule: persistent warps over contiguous tile ranges with incremental
+//   tile cursors (tile128.cuh).
 #include <cuda.h>
 #include <stdint.h>
 #include <math.h>
