@@ -216,9 +216,10 @@ DCT16A_API int dct16a_zonal_sweep(const void* src, const dct16a_desc* desc, int3
  * same bytes).  Initial values come from the environment variables named
  * below; set_option returns DCT16A_EDOMAIN for an unknown option or value.
  *   DCT16A_OPT_CODEC_PATH (env DCT16A_CODEC_PATH): fused-codec kernel choice,
- *     0 = automatic (default): zonal 8-bit with r <= 36 on the thread-per-block
- *         kernel, everything else on the warp-per-block-pair kernel;
- *     1 = zonal on the generic kernel; 2 = always the warp-per-block-pair kernel.
+ *     0 = automatic (default): zonal 8-bit with r <= 36 on the band-pruned
+ *         warp-per-tile kernel, everything else on the warp-per-block-pair kernel;
+ *     1 = zonal on the generic kernel; 2 = always the warp-per-block-pair kernel;
+ *     3 = zonal 8-bit with r <= 36 on the thread-per-block kernel.
  *   DCT16A_OPT_FWD_STORE (env DCT16A_FWD_STORE): output path of the forward
  *     kernel, -1 = default, 0..5 = the variants of profiles/r01_fwd_store_modes.md.
  */

@@ -10,7 +10,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libdct16a.so")
-SOURCES = ["abi.cu", "forward.cu", "codec.cu", "zonal_tpb.cu", "codec_warp.cu", "sweep.cu", "ssim.cu"]
+SOURCES = ["abi.cu", "forward.cu", "codec.cu", "zonal_tpb.cu", "zonal_band.cu", "codec_warp.cu", "sweep.cu", "ssim.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v", "--expt-relaxed-constexpr",

@@ -296,7 +296,7 @@ DCT16A_API int dct16a_zonal_sweep(const void* src, const dct16a_desc* desc, int3
 
 DCT16A_API int dct16a_set_option(int option, int value) {
     if (option == DCT16A_OPT_CODEC_PATH) {
-        if (value < 0 || value > 2) return fail(DCT16A_EDOMAIN, "codec path %d not in [0, 2]", value);
+        if (value < 0 || value > 3) return fail(DCT16A_EDOMAIN, "codec path %d not in [0, 3]", value);
         g_codec_path.store(value);
         return DCT16A_OK;
     }

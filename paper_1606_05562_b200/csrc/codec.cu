@@ -402,18 +402,20 @@ int launch_codec_generic(const void* src, const Geom& g, const dct16a_quant& q, 
 }
 
 // Kernel choice of the fused codec (option DCT16A_OPT_CODEC_PATH, include/dct16a.h):
-//   0 auto: zonal 8-bit with r <= 36 -> thread-per-block kernel (zonal_tpb.cu),
+//   0 auto: zonal 8-bit with r <= 36 -> band-pruned warp kernel (zonal_band.cu),
 //           everything else -> warp-per-block-pair kernel (codec_warp.cu);
 //   1: zonal -> the generic kernel above (uniform stays on codec_warp.cu);
-//   2: always codec_warp.cu.
-// The three implementations are independent cross-checks of each other.
+//   2: always codec_warp.cu;
+//   3: zonal 8-bit with r <= 36 -> thread-per-block kernel (zonal_tpb.cu).
+// The four implementations are independent cross-checks of each other.
 int launch_codec(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse,
                  double* psnr, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(uint64_t) * g.N, st);
     if (e) return static_cast<int>(e);
     const int path = get_option(DCT16A_OPT_CODEC_PATH);
     int rc = 1;
-    if (q.mode == DCT16A_ZONAL && path == 0) rc = launch_zonal_tpb(src, g, q.r, recon, sse, st);
+    if (q.mode == DCT16A_ZONAL && path == 0) rc = launch_zonal_band(src, g, q.r, recon, sse, st);
+    if (q.mode == DCT16A_ZONAL && path == 3) rc = launch_zonal_tpb(src, g, q.r, recon, sse, st);
     if (rc == 1) {
         if (q.mode == DCT16A_ZONAL && path == 1) rc = launch_codec_generic(src, g, q, recon, sse, st);
         else rc = launch_codec_warp(src, g, q, recon, sse, st);

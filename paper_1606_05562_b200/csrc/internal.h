@@ -45,6 +45,7 @@ int launch_codec(const void* src, const Geom& g, const dct16a_quant& q, void* re
                  uint64_t* sse, double* psnr, cudaStream_t st);
 // thread-per-block zonal codec for 8-bit and small bands; returns 1 if not applicable
 int launch_zonal_tpb(const void* src, const Geom& g, int r, void* recon, uint64_t* sse, cudaStream_t st);
+int launch_zonal_band(const void* src, const Geom& g, int r, void* recon, uint64_t* sse, cudaStream_t st);
 int zonal_band(int r);
 // warp-per-block-pair codec (uniform, and zonal cases zonal_tpb does not take)
 int launch_codec_warp(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse,

@@ -107,12 +107,12 @@ def test_binding_rejects_cpu_tensors():
 
 def test_options_validate_and_round_trip():
     old = pkg.dct16a_get_option(pkg.OPT_CODEC_PATH)
-    for v in (0, 1, 2):
+    for v in (0, 1, 2, 3):
         pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, v)
         assert pkg.dct16a_get_option(pkg.OPT_CODEC_PATH) == v
     pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, old)
     with pytest.raises(pkg.Dct16aError) as e:
-        pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, 3)
+        pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, 4)
     assert e.value.code == -5
     with pytest.raises(pkg.Dct16aError) as e:
         pkg.dct16a_set_option(99, 0)

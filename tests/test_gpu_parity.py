@@ -191,11 +191,11 @@ def test_psnr_kernel():
     assert sse.cpu().tolist() == oc.sse(a, b, 32)
 
 
-@pytest.fixture(params=[0, 1, 2], ids=["auto", "generic", "warp"])
+@pytest.fixture(params=[0, 1, 2, 3], ids=["auto", "generic", "warp", "tpb"])
 def codec_path(request):
     """Every fused-codec test runs on each kernel choice (DCT16A_OPT_CODEC_PATH):
-    the thread-per-block, generic and warp-per-block-pair kernels are checked
-    against the oracle independently."""
+    the band-pruned warp-per-tile, generic, warp-per-block-pair and
+    thread-per-block kernels are checked against the oracle independently."""
     old = pkg.dct16a_get_option(pkg.OPT_CODEC_PATH)
     pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, request.param)
     yield request.param
@@ -220,7 +220,7 @@ def test_codec_config1(codec_path):
 
 @pytest.mark.parametrize("r", [1, 2, 10, 11, 16, 21, 22, 32, 36, 37, 100, 256])
 def test_codec_zonal_varied(r, codec_path):
-    # r <= 36 runs the thread-per-block kernel (bands 3/5/7), larger r the generic one
+    # r <= 36 runs the band-pruned kernels (bands 3/5/7), larger r the warp-per-block-pair one
     imgs = np.concatenate([synth.batch_u8([40, 41], 48, 272), synth.adversarial_u8(48, 272)])
     _codec_check(imgs, "zonal", 8, r=r)
 
@@ -676,7 +676,7 @@ def test_random_shapes_every_entry(seed):
     step = int(rng.integers(1, 100))
     old = pkg.dct16a_get_option(pkg.OPT_CODEC_PATH)
     try:
-        for path in (0, 1, 2):
+        for path in (0, 1, 2, 3):
             pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, path)
             for mode in ("zonal", "uniform"):
                 rec, sse, _ = pkg.codec(t, mode, r=r, step=step)

@@ -39,7 +39,7 @@ def main():
             ps = torch.empty(n, dtype=torch.float64, device=dev)
             pkg.dct16a_psnr(x.contiguous(), rec, sse, ps, pkg.desc_of(rec, bd))
             chk += int(sse.sum())
-            for path in (0, 1, 2):
+            for path in (0, 1, 2, 3):
                 pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, path)
                 for r2 in (16, 40):
                     rec2, sse2, _ = pkg.codec(x.contiguous(), mode, r=r2, step=step)
