@@ -19,13 +19,16 @@
 //   rows, outputs k <= BAND; Z_00 in [0, 65280] is decoded unsigned, every other
 //   Z in int16 (the K1 ranges).  W = 2304/(g_k g_l) on the zonal cells, the
 //   rounding offset 1152 on the DC input: every pixel of the inverse is N + 1152.
-// * Inverse in int32 (exact: |N| < 2^23 for 8-bit input): lane (b, p) runs the
-//   transposed network down its two columns (inputs k <= BAND), the smem tile
-//   turns columns into rows, lane (b, q) runs rows q, q+4, q+8, q+12 (inputs
-//   l <= BAND).  pixel = floor((N + 1152)/2304) by one I2F and one round-down
-//   FMA onto 2^23 (exact: fl(1/2304) > 1/2304 with relative error 7.5e-9, so
-//   for 0 <= x < 2^23 the product never falls below an integer it should reach
-//   nor reaches one it should not; negative results saturate to 0 in the pack).
+// * Inverse in float32, exact: every input W·Z (+1152) and every partial sum is
+//   an integer of magnitude < 2^23 for 8-bit input (sum of W·|Z| over the band
+//   <= sqrt(sum W)·sqrt(2304·sum X²) < 7.1e6).  Lane (b, p) runs the transposed
+//   network down its two columns (inputs k <= BAND, the others compile-time
+//   zeros), the smem tile turns columns into rows, lane (b, q) runs rows q, q+4,
+//   q+8, q+12 (inputs l <= BAND).  pixel = floor((N + 1152)/2304) by one
+//   round-down FMA onto 2^23 (exact: fl(1/2304) > 1/2304 with relative error
+//   7.5e-9, so for 0 <= x < 2^23 the product never falls below an integer it
+//   should reach nor reaches one it should not; negative results saturate to 0
+//   in the pack).
 // * SSE per row: cvt.pack.sat + vabsdiff4 + dp4a against the original bytes;
 //   the reconstruction overwrites the tile in place and leaves by TMA store.
 #include <cuda.h>
@@ -50,16 +53,26 @@ namespace {
 constexpr int kBWarps = 4;
 constexpr int kBStages = DCT16A_ZB_STAGES;
 constexpr int kBStage = 16 * 128;   // one u8 tile
-// per-warp transposition words: ty[8 blocks][16 rows][4 column-pair words]
-// (block stride 68) and tu[8 blocks][16 rows][8 int32] (block stride 132) share
-// one buffer; the strides put the 8 blocks of a quarter-warp on distinct banks
-constexpr int kTyBlock = 68;
-constexpr int kTuBlock = 132;
-constexpr int kBXpose = 5120;   // >= 8·132·4 = 4224 B, keeps every stage 1024-byte aligned
+// per-warp transposition buffers (32-bit words), sharing one region:
+//   ty[4 block pairs][16 rows][8 SWAR words], row pitch 12, pair stride 200;
+//   tu[4 block pairs][16 rows][8 columns][2 blocks] float, row pitch 20, pair stride 336.
+// The pitches and strides put the lanes of every shared-memory phase on distinct banks.
+constexpr int kTyRow = 12, kTyBlock = 200;
+constexpr int kTuRow = 20, kTuBlock = 336;
+constexpr int kBXpose = 6144;   // >= 4·336·4 = 5376 B, keeps every stage 1024-byte aligned
 constexpr int kBWarpBytes = kBStages * kBStage + kBXpose;
 static_assert(kBWarpBytes % 1024 == 0, "stages must stay 1024-byte aligned");
-static_assert(8 * kTuBlock * 4 <= kBXpose, "transposition buffer too small");
+static_assert(4 * kTuBlock * 4 <= kBXpose && 4 * kTyBlock * 4 <= kBXpose, "transposition buffer too small");
 constexpr int kBSmem = 1024 + kBWarps * kBWarpBytes + kBWarps * kBStages * 8;
+
+// two float32 lanes processed by one FADD2/FFMA2 (sm_100): the two blocks of a pair
+struct F2 {
+    float2 v;
+};
+__device__ __forceinline__ F2 operator+(F2 a, F2 b) { return F2{__fadd2_rn(a.v, b.v)}; }
+__device__ __forceinline__ F2 operator-(F2 a, F2 b) { return F2{__fadd2_rn(a.v, make_float2(-b.v.x, -b.v.y))}; }
+__device__ __forceinline__ F2 operator-(F2 a) { return F2{make_float2(-a.v.x, -a.v.y)}; }
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) { return F2{__ffma2_rn(a.v, b.v, c.v)}; }
 
 struct BParams {
     int W, BX, BY, VH, tiles_per_strip;
@@ -74,7 +87,6 @@ template <int BAND>
 __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
     zband_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
                  unsigned long long* __restrict__ sse, const BParams p) {
-    constexpr int NP = BAND / 2 + 1;   // column pairs covering l <= BAND (BAND odd)
     static_assert(BAND % 2 == 1 && BAND <= 7, "BAND must be 3, 5 or 7");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = walign1024(smem_raw);
@@ -104,21 +116,25 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
     }
     __syncwarp();
 
-    const int b = lane & 7;    // block of the tile
-    const int q = lane >> 3;   // row quarter (row and pixel passes) / column pair (column pass)
-    // column pass constants: weights of columns 2q, 2q+1 (0 outside the zonal set)
-    int w0[BAND + 1], w1s[BAND + 1];
+    // lane = (block pair bp = lane >> 3: blocks bp and bp + 4 of the tile, r8 = lane & 7)
+    const int bp = lane >> 3;
+    const int r8 = lane & 7;   // rows r8, r8 + 8 (row and pixel passes) / column l = r8 (column pass)
+    const int l = r8;
+    // column pass constants: the weight of column l on both SWAR lanes (the high
+    // lane arrives as Z·2^16, so its weight carries 2^-16: an exact scaling)
+    F2 wl[BAND + 1];
 #pragma unroll
     for (int k = 0; k <= BAND; ++k) {
-        w0[k] = zigzag_rank(k, 2 * q) < p.r ? w_of(k, 2 * q) : 0;
-        w1s[k] = zigzag_rank(k, 2 * q + 1) < p.r ? (w_of(k, 2 * q + 1) << 16) : 0;   // ·2^16 for mulhi
+        const float w = zigzag_rank(k, l) < p.r ? static_cast<float>(w_of(k, l)) : 0.0f;
+        wl[k] = F2{make_float2(w, w * 0x1p-16f)};
     }
-    const bool dc_unsigned = q == 0;                       // Z_00 in [0, 65280] is decoded unsigned
-    const int dc_off = q == 0 ? 1152 : 0;                  // rounding offset on the DC input
-    const float inv2304 = 1.0f / 2304.0f;
+    const bool dc_lane = l == 0;                                       // Z_00 in [0, 65280]: unsigned
+    const F2 dc_off{make_float2(dc_lane ? 1152.0f : 0.0f, dc_lane ? 1152.0f : 0.0f)};   // rounding offset
+    const F2 inv2304{make_float2(1.0f / 2304.0f, 1.0f / 2304.0f)};
+    const F2 two23{make_float2(8388608.0f, 8388608.0f)};
 
-    uint32_t* ty = xp + b * kTyBlock;
-    uint32_t* tu = xp + b * kTuBlock;
+    uint32_t* ty = xp + bp * kTyBlock;
+    float* tu = reinterpret_cast<float*>(xp) + bp * kTuBlock;
 
     unsigned long long acc = 0;
     int cur_n = -1;
@@ -138,14 +154,15 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
             acc = 0;
             cur_n = n;
         }
-        const bool bvalid = x0 / 16 + b < p.BX;
+        const bool valid0 = x0 / 16 + bp < p.BX;
+        const bool valid1 = x0 / 16 + bp + 4 < p.BX;
 
-        // ---- row pass: rows (q + 4pr, q + 4pr + 8) as one SWAR vector, outputs l <= BAND
+        // ---- row pass: row t of blocks bp and bp + 4 as one SWAR vector, outputs l <= BAND
 #pragma unroll
-        for (int pr = 0; pr < 2; ++pr) {
-            const int t = q + 4 * pr;
-            const uint4 A = *reinterpret_cast<const uint4*>(stage + swz(t, b));
-            const uint4 B = *reinterpret_cast<const uint4*>(stage + swz(t + 8, b));
+        for (int h = 0; h < 2; ++h) {
+            const int t = r8 + 8 * h;
+            const uint4 A = *reinterpret_cast<const uint4*>(stage + swz(t, bp));
+            const uint4 B = *reinterpret_cast<const uint4*>(stage + swz(t, bp + 4));
             const uint32_t a[4] = {A.x, A.y, A.z, A.w};
             const uint32_t bw[4] = {B.x, B.y, B.z, B.w};
             uint32_t x[16], y[16];
@@ -159,97 +176,81 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
                 x[4 * c + 3] = __byte_perm(v, 0u, 0x4341);
             }
             net_fwd(x, y);
-            uint32_t ra[NP], rb[NP];
-#pragma unroll
-            for (int pp = 0; pp < NP; ++pp) {
-                // |Y| <= 4080: +2^15 per lane keeps both halves non-negative, so each
-                // half is the exact biased value and PRMT can regroup them
-                const uint32_t y0 = y[2 * pp] + 0x80008000u, y1 = y[2 * pp + 1] + 0x80008000u;
-                ra[pp] = __byte_perm(y0, y1, 0x5410);   // row t:     (Y[t][2pp], Y[t][2pp+1])
-                rb[pp] = __byte_perm(y0, y1, 0x7632);   // row t + 8
-            }
-            if constexpr (NP == 4) {
-                *reinterpret_cast<uint4*>(ty + t * 4) = make_uint4(ra[0], ra[1], ra[2], ra[3]);
-                *reinterpret_cast<uint4*>(ty + (t + 8) * 4) = make_uint4(rb[0], rb[1], rb[2], rb[3]);
-            } else {
-#pragma unroll
-                for (int pp = 0; pp < NP; ++pp) {
-                    ty[t * 4 + pp] = ra[pp];
-                    ty[(t + 8) * 4 + pp] = rb[pp];
-                }
+            // the SWAR words go to the column pass as they are (lo + hi·2^16 mod 2^32)
+            *reinterpret_cast<uint4*>(ty + t * kTyRow) = make_uint4(y[0], y[1], y[2], y[3]);
+            if constexpr (BAND >= 7) {
+                *reinterpret_cast<uint4*>(ty + t * kTyRow + 4) = make_uint4(y[4], y[5], y[6], y[7]);
+            } else if constexpr (BAND >= 5) {
+                *reinterpret_cast<uint2*>(ty + t * kTyRow + 4) = make_uint2(y[4], y[5]);
             }
         }
         __syncwarp();
 
-        // ---- column pass on column pair (2q, 2q+1), outputs k <= BAND; weights; inverse down the columns
+        // ---- column pass on column l of both blocks, outputs k <= BAND; weights; inverse down the column
         {
             uint32_t cw[16], z[16];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) cw[k] = ty[k * 4 + q];
+            for (int t = 0; t < 16; ++t) cw[t] = ty[t * kTyRow + l];
             __syncwarp();   // every lane has read ty before tu (same buffer) is written
             net_fwd(cw, z);
-            int c0[16], c1[16];
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                c0[k] = 0;
-                c1[k] = 0;
-            }
+            F2 c[16];
 #pragma unroll
             for (int k = 0; k <= BAND; ++k) {
-                // the 2^15 input bias adds 2^15·(sum of row k of T) per lane: 2^19 for k = 0, 0 otherwise
-                const uint32_t wd = k == 0 ? z[0] - 0x00080000u : z[k];
-                const int lo = k == 0 && dc_unsigned ? static_cast<int>(wd & 0xFFFFu)
-                                                     : static_cast<int>(static_cast<int16_t>(wd & 0xFFFFu));
-                const int hs = static_cast<int>(wd - static_cast<uint32_t>(lo));   // Z_hi·2^16
-                c0[k] = lo * w0[k] + (k == 0 ? dc_off : 0);
-                c1[k] = __mulhi(hs, w1s[k]);                                      // Z_hi·W
+                // z[k] = Z_lo + Z_hi·2^16 (mod 2^32); Z_00 in [0, 65280], every other Z in int16
+                const bool uns = k == 0 && dc_lane;
+                const int lo = uns ? static_cast<int>(z[k] & 0xFFFFu) : static_cast<int>(static_cast<int16_t>(z[k] & 0xFFFFu));
+                const uint32_t hs = z[k] - static_cast<uint32_t>(lo);   // Z_hi·2^16
+                const float hf = uns ? static_cast<float>(hs) : static_cast<float>(static_cast<int>(hs));
+                // exact in float: W·Z + 1152 and every later partial sum are integers below 2^23
+                c[k] = fma2(F2{make_float2(static_cast<float>(lo), hf)}, wl[k], k == 0 ? dc_off : F2{make_float2(0.0f, 0.0f)});
             }
-            int u0[16], u1[16];
-            net_inv(c0, u0);
-            net_inv(c1, u1);
+            F2 u[16];
+            net_inv_head<BAND + 1>(c, u);
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-                *reinterpret_cast<int2*>(tu + i * 8 + 2 * q) = make_int2(u0[i], u1[i]);
+            for (int i = 0; i < 16; ++i) *reinterpret_cast<float2*>(tu + i * kTuRow + 2 * l) = u[i].v;
         }
         __syncwarp();
 
-        // ---- inverse along the rows q, q+4, q+8, q+12, pixels, SSE, in-place reconstruction
+        // ---- inverse along row i of both blocks, pixels, SSE, in-place reconstruction
 #pragma unroll
-        for (int s4 = 0; s4 < 4; ++s4) {
-            const int i = q + 4 * s4;
-            int v[16], a[16];
+        for (int h = 0; h < 2; ++h) {
+            const int i = r8 + 8 * h;
+            F2 v[16], a[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = 0;
-            {
-                const int4 v0 = *reinterpret_cast<const int4*>(tu + i * 8);
-                v[0] = v0.x; v[1] = v0.y; v[2] = v0.z; v[3] = v0.w;
-                if (BAND >= 4) {
-                    const int4 v1 = *reinterpret_cast<const int4*>(tu + i * 8 + 4);
-                    v[4] = v1.x; v[5] = v1.y;
-                    if (BAND >= 6) { v[6] = v1.z; v[7] = v1.w; }
+            for (int j = 0; j <= BAND; j += 2) {
+                const float4 q4 = *reinterpret_cast<const float4*>(tu + i * kTuRow + 2 * j);
+                v[j] = F2{make_float2(q4.x, q4.y)};
+                v[j + 1] = F2{make_float2(q4.z, q4.w)};
+            }
+            net_inv_head<BAND + 1>(v, a);
+            int pa[16], pb[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                // floor((N + 1152)/2304) for both blocks by one round-down FMA onto 2^23
+                const float2 r = __ffma2_rd(a[j].v, inv2304.v, two23.v);
+                pa[j] = static_cast<int>(__float_as_uint(r.x) - 0x4B000000u);
+                pb[j] = static_cast<int>(__float_as_uint(r.y) - 0x4B000000u);
+            }
+            const bool row_ok = by * 16 + i < p.VH;
+#pragma unroll
+            for (int blk = 0; blk < 2; ++blk) {
+                const int* pv = blk ? pb : pa;
+                uint32_t o[4];
+#pragma unroll
+                for (int c4 = 0; c4 < 4; ++c4)
+                    o[c4] = pack2_sat_u8(pv[4 * c4 + 1], pv[4 * c4], pack2_sat_u8(pv[4 * c4 + 3], pv[4 * c4 + 2], 0u));
+                uint4* cell = reinterpret_cast<uint4*>(stage + swz(i, bp + 4 * blk));
+                const uint4 orig = *cell;
+                const uint32_t ow[4] = {orig.x, orig.y, orig.z, orig.w};
+                uint32_t e = 0;
+#pragma unroll
+                for (int c4 = 0; c4 < 4; ++c4) {
+                    const uint32_t dd = __vabsdiffu4(o[c4], ow[c4]);
+                    e = __dp4a(dd, dd, e);
                 }
+                if ((blk ? valid1 : valid0) && row_ok) acc += e;
+                if (p.has_recon) *cell = make_uint4(o[0], o[1], o[2], o[3]);
             }
-            net_inv(v, a);
-            int pv[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                pv[j] = static_cast<int>(__float_as_uint(__fmaf_rd(static_cast<float>(a[j]), inv2304, 8388608.0f)) -
-                                         0x4B000000u);
-            uint32_t o[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-                o[c] = pack2_sat_u8(pv[4 * c + 1], pv[4 * c], pack2_sat_u8(pv[4 * c + 3], pv[4 * c + 2], 0u));
-            uint4* cell = reinterpret_cast<uint4*>(stage + swz(i, b));
-            const uint4 orig = *cell;
-            uint32_t e = 0;
-            const uint32_t ow[4] = {orig.x, orig.y, orig.z, orig.w};
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const uint32_t dd = __vabsdiffu4(o[c], ow[c]);
-                e = __dp4a(dd, dd, e);
-            }
-            if (bvalid && by * 16 + i < p.VH) acc += e;
-            if (p.has_recon) *cell = make_uint4(o[0], o[1], o[2], o[3]);
         }
         __syncwarp();
         if (lane == 0) {
