@@ -15,7 +15,8 @@
 // pass, smem transposition, column pass (lane = column l) producing W ⊙ Z into
 // smem, then the sweep with lane = row i: N[i][:] += (W·Z_kl·T_ki)·T_l[:] in
 // float32 (exact: half-integers below 2^23, the +1152.5 rounding offset rides
-// in N from the start), pixel = floor(N/2304) by one round-down FMA, clamp,
+// in N from the start; two columns per FFMA2), pixel = floor(N/2304) by one
+// round-down FMA (FFMA2.RM for a column pair), clamp,
 // squared error in float32 (exact below 2^24 per row), one REDUX per r and a
 // shared-memory 64-bit atomic into the warp's per-r SSE, flushed to global per
 // image.
@@ -184,9 +185,10 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
             }
             __syncwarp();
             // ---- the sweep, lane = row i = t
-            float N[16];
+            // N[i][2m], N[i][2m+1] as one float2: the update and the rounding are FFMA2
+            float2 N[8];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) N[j] = 1152.5f;
+            for (int m = 0; m < 8; ++m) N[m] = make_float2(1152.5f, 1152.5f);
             // operands of the rank-1 step r (zig-zag cell of rank r-1), prefetched one step ahead
             float sv;
             float4 tq[4];
@@ -198,14 +200,14 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
                 for (int q = 0; q < 4; ++q) t_out[q] = tr[q];
             };
             auto update = [&]() {
+                const float2 s2 = make_float2(sv, sv);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    N[4 * q] = fmaf(sv, tq[q].x, N[4 * q]);
-                    N[4 * q + 1] = fmaf(sv, tq[q].y, N[4 * q + 1]);
-                    N[4 * q + 2] = fmaf(sv, tq[q].z, N[4 * q + 2]);
-                    N[4 * q + 3] = fmaf(sv, tq[q].w, N[4 * q + 3]);
+                    N[2 * q] = __ffma2_rn(s2, make_float2(tq[q].x, tq[q].y), N[2 * q]);
+                    N[2 * q + 1] = __ffma2_rn(s2, make_float2(tq[q].z, tq[q].w), N[2 * q + 1]);
                 }
             };
+            const float2 inv2 = make_float2(inv2304, inv2304), m2 = make_float2(8388608.0f, 8388608.0f);
             fetch(1, sv, tq);
 #pragma unroll 1
             for (int r = 1; r < p.r_first; ++r) {   // below the requested range: update only
@@ -231,24 +233,25 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
                     ei = 0;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        int v[4];
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            v[i] = static_cast<int>(__float_as_uint(__fmaf_rd(N[4 * q + i], inv2304, 8388608.0f)) -
-                                                    0x4B000000u);
+                        const float2 f0 = __ffma2_rd(N[2 * q], inv2, m2), f1 = __ffma2_rd(N[2 * q + 1], inv2, m2);
+                        const int v[4] = {static_cast<int>(__float_as_uint(f0.x) - 0x4B000000u),
+                                          static_cast<int>(__float_as_uint(f0.y) - 0x4B000000u),
+                                          static_cast<int>(__float_as_uint(f1.x) - 0x4B000000u),
+                                          static_cast<int>(__float_as_uint(f1.y) - 0x4B000000u)};
                         const uint32_t pk = pack2_sat_u8(v[1], v[0], pack2_sat_u8(v[3], v[2], 0u));
                         const uint32_t d = __vabsdiffu4(pk, xw[q]);
                         ei = __dp4a(d, d, ei);
                     }
                 } else {
-                    float e = 0.0f;
+                    float2 e2 = make_float2(0.0f, 0.0f);
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const float f = fminf(fmaxf(__fmaf_rd(N[j], inv2304, 8388608.0f), 8388608.0f), top);
-                        const float d = f - xs[j];
-                        e = fmaf(d, d, e);
+                    for (int m = 0; m < 8; ++m) {
+                        const float2 f = __ffma2_rd(N[m], inv2, m2);
+                        const float2 fc = make_float2(fminf(fmaxf(f.x, 8388608.0f), top), fminf(fmaxf(f.y, 8388608.0f), top));
+                        const float2 d = __fadd2_rn(fc, make_float2(-xs[2 * m], -xs[2 * m + 1]));
+                        e2 = __ffma2_rn(d, d, e2);
                     }
-                    ei = __float2uint_rn(e);
+                    ei = __float2uint_rn(e2.x + e2.y);
                 }
                 const unsigned tot = __reduce_add_sync(0xffffffffu, contributes ? ei : 0u);
                 if (lane == 0) ssew[r - p.r_first] += tot;   // this warp's own accumulator: no atomic
