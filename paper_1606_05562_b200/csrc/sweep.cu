@@ -15,8 +15,10 @@
 // pass, smem transposition, column pass (lane = column l) producing W ⊙ Z into
 // smem, then the sweep with lane = row i: N[i][:] += (W·Z_kl·T_ki)·T_l[:] in
 // float32 (exact: half-integers below 2^23, the +1152.5 rounding offset rides
-// in N from the start; two columns per FFMA2), pixel = floor(N/2304) by one
-// round-down FMA (FFMA2.RM for a column pair), clamp,
+// in N from the start; two columns per FFMA2; N is held as N·2^-35),
+// pixel = floor(N/2304) by one round-down multiply into the subnormal range
+// whose bits are the integer (8-bit; zonal_band.cu) or one round-down FMA onto
+// 2^23 (10-bit), clamp,
 // squared error in float32 (exact below 2^24 per row), one REDUX per r and a
 // shared-memory 64-bit atomic into the warp's per-r SSE, flushed to global per
 // image.
@@ -119,10 +121,12 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
 
     // per-lane weights of column l = t by class of k: W = 2304/(g_k·g_l)
     const int l = t;
-    const float w16 = static_cast<float>(2304 / (16 * g_of(l)));
-    const float w12 = static_cast<float>(2304 / (12 * g_of(l)));
-    const float w8 = static_cast<float>(2304 / (8 * g_of(l)));
-    const float inv2304 = 1.0f / 2304.0f;
+    // N is carried as N·2^-35 (exact: half-integers below 2^23 times a power of two),
+    // so the 8-bit rounding can land its integer in the subnormal bits (header)
+    const float w16 = static_cast<float>(2304 / (16 * g_of(l))) * 0x1p-35f;
+    const float w12 = static_cast<float>(2304 / (12 * g_of(l))) * 0x1p-35f;
+    const float w8 = static_cast<float>(2304 / (8 * g_of(l))) * 0x1p-35f;
+    const float inv2304 = 0x1p35f / 2304.0f;   // 10-bit: floor onto 2^23 of N·2^-35 · 2^35/2304
     const float top = 8388608.0f + static_cast<float>(p.maxpix);
 
     int cur_n = -1;
@@ -188,7 +192,7 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
             // N[i][2m], N[i][2m+1] as one float2: the update and the rounding are FFMA2
             float2 N[8];
 #pragma unroll
-            for (int m = 0; m < 8; ++m) N[m] = make_float2(1152.5f, 1152.5f);
+            for (int m = 0; m < 8; ++m) N[m] = make_float2(1152.5f * 0x1p-35f, 1152.5f * 0x1p-35f);
             // operands of the rank-1 step r (zig-zag cell of rank r-1), prefetched one step ahead
             float sv;
             float4 tq[4];
@@ -208,6 +212,7 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
                 }
             };
             const float2 inv2 = make_float2(inv2304, inv2304), m2 = make_float2(8388608.0f, 8388608.0f);
+            const float2 pix2 = make_float2(0x1p-114f / 2304.0f, 0x1p-114f / 2304.0f);
             fetch(1, sv, tq);
 #pragma unroll 1
             for (int r = 1; r < p.r_first; ++r) {   // below the requested range: update only
@@ -233,11 +238,11 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
                     ei = 0;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const float2 f0 = __ffma2_rd(N[2 * q], inv2, m2), f1 = __ffma2_rd(N[2 * q + 1], inv2, m2);
-                        const int v[4] = {static_cast<int>(__float_as_uint(f0.x) - 0x4B000000u),
-                                          static_cast<int>(__float_as_uint(f0.y) - 0x4B000000u),
-                                          static_cast<int>(__float_as_uint(f1.x) - 0x4B000000u),
-                                          static_cast<int>(__float_as_uint(f1.y) - 0x4B000000u)};
+                        // (N·2^-35)·fl(2^-114/2304) rounded down to the subnormal grid:
+                        // the bits are floor(N·fl(1/2304)) (negative -> sign bit -> 0)
+                        const float2 f0 = __fmul2_rd(N[2 * q], pix2), f1 = __fmul2_rd(N[2 * q + 1], pix2);
+                        const int v[4] = {__float_as_int(f0.x), __float_as_int(f0.y), __float_as_int(f1.x),
+                                          __float_as_int(f1.y)};
                         const uint32_t pk = pack2_sat_u8(v[1], v[0], pack2_sat_u8(v[3], v[2], 0u));
                         const uint32_t d = __vabsdiffu4(pk, xw[q]);
                         ei = __dp4a(d, d, ei);

@@ -19,16 +19,20 @@
 //   rows, outputs k <= BAND; Z_00 in [0, 65280] is decoded unsigned, every other
 //   Z in int16 (the K1 ranges).  W = 2304/(g_k g_l) on the zonal cells, the
 //   rounding offset 1152 on the DC input: every pixel of the inverse is N + 1152.
-// * Inverse in float32, exact: every input W·Z (+1152) and every partial sum is
-//   an integer of magnitude < 2^23 for 8-bit input (sum of W·|Z| over the band
-//   <= sqrt(sum W)·sqrt(2304·sum X²) < 7.1e6).  Lane (b, p) runs the transposed
-//   network down its two columns (inputs k <= BAND, the others compile-time
-//   zeros), the smem tile turns columns into rows, lane (b, q) runs rows q, q+4,
-//   q+8, q+12 (inputs l <= BAND).  pixel = floor((N + 1152)/2304) by one
-//   round-down FMA onto 2^23 (exact: fl(1/2304) > 1/2304 with relative error
-//   7.5e-9, so for 0 <= x < 2^23 the product never falls below an integer it
-//   should reach nor reaches one it should not; negative results saturate to 0
-//   in the pack).
+// * Inverse in float32, exact, on N·2^-35: every input W·Z (+1152) and every
+//   partial sum is an integer of magnitude < 2^23 for 8-bit input (sum of W·|Z|
+//   over the band <= sqrt(sum W)·sqrt(2304·sum X²) < 7.1e6) times 2^-35, so every
+//   value is a normal float held exactly.  Lane (bp, l) runs the transposed
+//   network down column l of both blocks (FADD2; inputs k <= BAND, the others
+//   compile-time zeros), the smem tile turns columns into rows, lane (bp, r8)
+//   runs rows r8, r8+8 of both blocks (inputs l <= BAND).
+// * Pixel = floor((N + 1152)/2304) by ONE round-down multiply per two pixels
+//   (FMUL2.RM) with c = fl(2^-114/2304): the exact product (N/2304)·2^-149·(1+δ)
+//   rounded down to the subnormal grid is floor(N·fl(1/2304))·2^-149, whose bit
+//   pattern is that integer (IEEE subnormals, no flush-to-zero).  fl(1/2304) >
+//   1/2304 with relative error δ = 7.5e-9, so for 0 <= N < 2^23 the floor is
+//   exact; a negative N gives a negative int (sign bit) and saturates to 0 in
+//   cvt.pack.sat, as a pixel above 255 saturates to 255.
 // * SSE per row: cvt.pack.sat + vabsdiff4 + dp4a against the original bytes;
 //   the reconstruction overwrites the tile in place and leaves by TMA store.
 #include <cuda.h>
@@ -125,13 +129,15 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
     F2 wl[BAND + 1];
 #pragma unroll
     for (int k = 0; k <= BAND; ++k) {
-        const float w = zigzag_rank(k, l) < p.r ? static_cast<float>(w_of(k, l)) : 0.0f;
+        // the whole inverse runs on N·2^-35 (header): the scaling rides in the weights
+        const float w = zigzag_rank(k, l) < p.r ? static_cast<float>(w_of(k, l)) * 0x1p-35f : 0.0f;
         wl[k] = F2{make_float2(w, w * 0x1p-16f)};
     }
     const bool dc_lane = l == 0;                                       // Z_00 in [0, 65280]: unsigned
-    const F2 dc_off{make_float2(dc_lane ? 1152.0f : 0.0f, dc_lane ? 1152.0f : 0.0f)};   // rounding offset
-    const F2 inv2304{make_float2(1.0f / 2304.0f, 1.0f / 2304.0f)};
-    const F2 two23{make_float2(8388608.0f, 8388608.0f)};
+    const float off = dc_lane ? 1152.0f * 0x1p-35f : 0.0f;             // rounding offset on the DC input
+    const F2 dc_off{make_float2(off, off)};
+    // fl(2^-114/2304) = 2^-114·fl(1/2304): N·2^-35 times it is (N/2304)·2^-149 (up to fl)
+    const F2 pix_scale{make_float2(0x1p-114f / 2304.0f, 0x1p-114f / 2304.0f)};
 
     uint32_t* ty = xp + bp * kTyBlock;
     float* tu = reinterpret_cast<float*>(xp) + bp * kTuBlock;
@@ -226,10 +232,11 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
             int pa[16], pb[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-                // floor((N + 1152)/2304) for both blocks by one round-down FMA onto 2^23
-                const float2 r = __ffma2_rd(a[j].v, inv2304.v, two23.v);
-                pa[j] = static_cast<int>(__float_as_uint(r.x) - 0x4B000000u);
-                pb[j] = static_cast<int>(__float_as_uint(r.y) - 0x4B000000u);
+                // floor((N + 1152)/2304) for both blocks by one round-down multiply into
+                // the subnormal range: the bits of the result are the integer itself
+                const float2 r = __fmul2_rd(a[j].v, pix_scale.v);
+                pa[j] = __float_as_int(r.x);
+                pb[j] = __float_as_int(r.y);
             }
             const bool row_ok = by * 16 + i < p.VH;
 #pragma unroll
