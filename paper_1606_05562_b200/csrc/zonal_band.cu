@@ -38,6 +38,8 @@
 #include <cuda.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "internal.h"
 #include "net16.cuh"
 #include "ptx.cuh"
@@ -49,7 +51,7 @@ namespace dct16a {
 namespace {
 
 #ifndef DCT16A_ZB_STAGES
-#define DCT16A_ZB_STAGES 3
+#define DCT16A_ZB_STAGES 4
 #endif
 #ifndef DCT16A_ZB_CTAS
 #define DCT16A_ZB_CTAS 4
@@ -63,11 +65,13 @@ constexpr int kBStage = 16 * 128;   // one u8 tile
 // The pitches and strides put the lanes of every shared-memory phase on distinct banks.
 constexpr int kTyRow = 12, kTyBlock = 200;
 constexpr int kTuRow = 20, kTuBlock = 336;
-constexpr int kBXpose = 6144;   // >= 4·336·4 = 5376 B, keeps every stage 1024-byte aligned
-constexpr int kBWarpBytes = kBStages * kBStage + kBXpose;
-static_assert(kBWarpBytes % 1024 == 0, "stages must stay 1024-byte aligned");
-static_assert(4 * kTuBlock * 4 <= kBXpose && 4 * kTyBlock * 4 <= kBXpose, "transposition buffer too small");
-constexpr int kBSmem = 1024 + kBWarps * kBWarpBytes + kBWarps * kBStages * 8;
+constexpr int kBXpose = 4 * kTuBlock * 4;   // 5376 B per warp
+static_assert(4 * kTyBlock * 4 <= kBXpose, "transposition buffer too small");
+// CTA smem: [every warp's TMA stages (1024-byte aligned: the swizzle takes address
+// bits 7-9)] [every warp's transposition buffer] [mbarriers]
+constexpr int kBWarpBytes = kBStages * kBStage;
+// + per warp: kBStages mbarriers and the coordinates (n, by, tb, valid) of the tile in each stage
+constexpr int kBSmem = 1024 + kBWarps * (kBWarpBytes + kBXpose) + kBWarps * kBStages * (8 + 16);
 
 // two float32 lanes processed by one FADD2/FFMA2 (sm_100): the two blocks of a pair
 struct F2 {
@@ -78,12 +82,26 @@ __device__ __forceinline__ F2 operator-(F2 a, F2 b) { return F2{__fadd2_rn(a.v, 
 __device__ __forceinline__ F2 operator-(F2 a) { return F2{make_float2(-a.v.x, -a.v.y)}; }
 __device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) { return F2{__ffma2_rn(a.v, b.v, c.v)}; }
 
+#ifndef DCT16A_ZB_CLAIM
+#define DCT16A_ZB_CLAIM 8
+#endif
+constexpr int kBClaim = DCT16A_ZB_CLAIM;   // consecutive tiles per claim
+
 struct BParams {
     int W, BX, BY, VH, tiles_per_strip;
-    long long n_tiles, chunk;   // tiles, tiles per warp
+    long long n_tiles;
     int r;
     int has_recon;
+    int slot, total_warps;   // dynamic tile scheduler
 };
+
+// Dynamic tile scheduler (as the forward kernel's, forward.cu): warps claim runs
+// of kBClaim consecutive tiles in increasing order from a global counter, so the
+// tiles in flight form one compact address window; 64 slots are used
+// round-robin by successive launches and the last warp of a launch resets its
+// slot (at most 64 concurrent launches per device).
+constexpr int kBSchedSlots = 64;
+__device__ unsigned long long g_zb_sched[kBSchedSlots][2];
 
 }  // namespace
 
@@ -97,26 +115,40 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     uint8_t* wbase = smem + warp * kBWarpBytes;
-    uint32_t* xp = reinterpret_cast<uint32_t*>(wbase + kBStages * kBStage);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBWarps * kBWarpBytes) + warp * kBStages;
+    uint32_t* xp = reinterpret_cast<uint32_t*>(smem + kBWarps * kBWarpBytes + warp * kBXpose);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBWarps * (kBWarpBytes + kBXpose)) + warp * kBStages;
 
-    const long long gw = static_cast<long long>(blockIdx.x) * kBWarps + warp;
-    const long long t0 = gw * p.chunk;
-    long long t1 = t0 + p.chunk;
-    if (t1 > p.n_tiles) t1 = p.n_tiles;
+    int4* coords = reinterpret_cast<int4*>(smem + kBWarps * (kBWarpBytes + kBXpose) + kBWarps * kBStages * 8) +
+                   warp * kBStages;
     const uint64_t pol = policy_evict_first();
+    unsigned long long* sched = g_zb_sched[p.slot];
 
+    // lane 0: the claim in progress (tiles [next, end)) and its cursor
+    long long next = 0, end = 0;
+    TileCursor ic;
+    // claim the next tile and issue its load into stage `st` (lane 0 only)
+    auto issue_next = [&](int st) {
+        if (next == end) {
+            const long long first = static_cast<long long>(atomicAdd(&sched[0], 1ull)) * kBClaim;
+            next = first;
+            end = first < p.n_tiles ? min(first + kBClaim, p.n_tiles) : first;
+            if (first < p.n_tiles) ic.init(p, first);
+        }
+        if (next < end) {
+            coords[st] = make_int4(ic.n, ic.by, ic.tb, 1);
+            w_issue_at<1>(&tin, p, ic, wbase + st * kBStage, &bars[st], pol);
+            ++next;
+            ic.advance(p);
+        } else {
+            coords[st] = make_int4(0, 0, 0, 0);
+        }
+    };
     if (lane == 0) {
-        for (int s = 0; s < kBStages; ++s) mbar_init(&bars[s], 1);
+        for (int st = 0; st < kBStages; ++st) mbar_init(&bars[st], 1);
         fence_mbar_init();
         prefetch_tmap(&tin);
         if (p.has_recon) prefetch_tmap(&tout);
-        TileCursor ic;
-        ic.init(p, t0);
-        for (int s = 0; s < kBStages - 1; ++s) {
-            if (t0 + s < t1) w_issue_at<1>(&tin, p, ic, wbase + s * kBStage, &bars[s], pol);
-            ic.advance(p);
-        }
+        for (int st = 0; st < kBStages - 1; ++st) issue_next(st);
     }
     __syncwarp();
 
@@ -144,14 +176,16 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
 
     unsigned long long acc = 0;
     int cur_n = -1;
-    int it = 0;
-    TileCursor cc, nc;   // the tile being consumed and the one kBStages - 1 ahead
-    cc.init(p, t0);
-    nc.init(p, t0 + kBStages - 1);
-    for (long long tix = t0; tix < t1; ++tix, ++it, cc.advance(p), nc.advance(p)) {
+    for (int it = 0;; ++it) {
         const int s = it % kBStages;
         uint8_t* stage = wbase + s * kBStage;
+        const int4 cd = coords[s];
+        if (!cd.w) break;   // claims only grow: every later stage is empty too
         mbar_wait(&bars[s], (it / kBStages) & 1);
+        TileCursor cc;
+        cc.n = cd.x;
+        cc.by = cd.y;
+        cc.tb = cd.z;
         const int n = cc.n, by = cc.by, x0 = cc.x0();
         if (n != cur_n) {   // image changed (warp-uniform): flush the previous image's SSE
 #pragma unroll
@@ -267,9 +301,7 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
                 bulk_commit();
                 bulk_wait_read<1>();   // the store of tile tix-1 has left the stage refilled next
             }
-            const long long nt = tix + kBStages - 1;
-            if (nt < t1) w_issue_at<1>(&tin, p, nc, wbase + ((it + kBStages - 1) % kBStages) * kBStage,
-                                       &bars[(it + kBStages - 1) % kBStages], pol);
+            issue_next((it + kBStages - 1) % kBStages);
         }
         __syncwarp();
     }
@@ -278,6 +310,11 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
     if (lane == 0) {
         if (acc) atomicAdd(sse + cur_n, acc);
         if (p.has_recon) bulk_wait<0>();
+        if (atomicAdd(&sched[1], 1ull) == static_cast<unsigned long long>(p.total_warps) - 1) {
+            // every warp has claimed past the end: reset the slot for a later launch
+            sched[0] = 0;
+            sched[1] = 0;
+        }
     }
 }
 
@@ -309,10 +346,12 @@ int launch_zb(const void* src, const Geom& g, int r, void* recon, uint64_t* sse,
     p.r = r;
     p.has_recon = recon != nullptr;
     if (int e = smem_optin(reinterpret_cast<const void*>(zband_kernel<BAND>), kBSmem)) return e;
-    long long warps = static_cast<long long>(num_sms()) * DCT16A_ZB_CTAS * kBWarps;
-    if (warps > p.n_tiles) warps = p.n_tiles;
-    p.chunk = (p.n_tiles + warps - 1) / warps;
-    const long long grid = (warps + kBWarps - 1) / kBWarps;
+    long long grid = static_cast<long long>(num_sms()) * DCT16A_ZB_CTAS;
+    const long long want = (p.n_tiles + kBWarps * kBClaim - 1) / (kBWarps * kBClaim);
+    if (want < grid) grid = want;
+    static std::atomic<unsigned> launch_seq{0};
+    p.slot = static_cast<int>(launch_seq.fetch_add(1) % kBSchedSlots);
+    p.total_warps = static_cast<int>(grid) * kBWarps;
     zband_kernel<BAND><<<static_cast<unsigned>(grid), kBWarps * 32, kBSmem, st>>>(
         tin, tout, reinterpret_cast<unsigned long long*>(sse), p);
     return static_cast<int>(cudaGetLastError());
