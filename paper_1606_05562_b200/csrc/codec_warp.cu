@@ -33,13 +33,15 @@
 // * SSE: per row, vabsdiff4/dp4a (8-bit) or integer squares (10-bit), one
 //   64-bit atomic per warp and image (or, for dct16a_codec_allreduce, into
 //   every rank's vector over peer memory).
-// * Schedule: persistent warps over contiguous tile ranges with incremental
-//   tile cursors (tile128.cuh).
+// * Schedule: persistent warps claim runs of consecutive tiles from a global
+//   counter (dynamic scheduler, compact address window) and walk each run with
+//   an incremental tile cursor (tile128.cuh).
 #include <cuda.h>
 #include <stdint.h>
 #include <math.h>
 #include <string.h>
 
+#include <atomic>
 #include <type_traits>
 
 #include "internal.h"
@@ -71,7 +73,8 @@ struct WCfg {
     static constexpr int kStageBytes = 16 * kWTile * 16 * ELEM;   // 2 KB (u8) / 4 KB (u16)
     static constexpr int kWarpBytes = kWStages * kStageBytes + kWXpose;
     static_assert(kWarpBytes % 1024 == 0, "stages must stay 1024-byte aligned");
-    static constexpr int kSmem = 1024 + kWWarps * kWarpBytes + kWWarps * kWStages * 8;
+    // + per warp: kWStages mbarriers and the coordinates (n, by, tb, valid) of each stage's tile
+    static constexpr int kSmem = 1024 + kWWarps * kWarpBytes + kWWarps * kWStages * (8 + 16);
     static constexpr int kFit = (227 * 1024) / (kSmem + 1024);
     // the float64 path needs ~170 registers: at most 3 CTAs (12 warps) per SM
     static constexpr int kCtasPerSm = UNIFORM ? (kFit < DCT16A_CW_UCTAS ? kFit : DCT16A_CW_UCTAS) : (kFit < 4 ? kFit : 4);
@@ -79,9 +82,21 @@ struct WCfg {
 
 constexpr int kMaxPeers = 8;
 
+#ifndef DCT16A_CW_CLAIM
+#define DCT16A_CW_CLAIM 4
+#endif
+constexpr int kWClaim = DCT16A_CW_CLAIM;   // consecutive tiles per claim
+// Dynamic tile scheduler (as in forward.cu / zonal_band.cu): runs of kWClaim
+// tiles claimed in increasing order from a global counter keep the tiles in
+// flight in one compact address window; 64 slots round-robin over launches,
+// reset by the last warp (at most 64 concurrent launches per device).
+constexpr int kWSchedSlots = 64;
+__device__ unsigned long long g_cw_sched[kWSchedSlots][2];
+
 struct WParams {
     int W, BX, BY, VH, tiles_per_strip, maxpix;
-    long long n_tiles, chunk;
+    long long n_tiles;
+    int slot, total_warps;
     int has_recon;
     // fused SSE all-reduce (dct16a_codec_allreduce): every image's SSE is added
     // into sse_peers[q][frame_offset + n] of every peer q; n_peers = 0: local sse
@@ -178,23 +193,36 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
     uint8_t* xpose = wbase + kWStages * Cfg::kStageBytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kWWarps * Cfg::kWarpBytes) + warp * kWStages;
 
-    const long long gw = static_cast<long long>(blockIdx.x) * kWWarps + warp;
-    const long long t0 = gw * p.chunk;
-    long long t1 = t0 + p.chunk;
-    if (t1 > p.n_tiles) t1 = p.n_tiles;
+    int4* coords = reinterpret_cast<int4*>(smem + kWWarps * Cfg::kWarpBytes + kWWarps * kWStages * 8) +
+                   warp * kWStages;
     const uint64_t pol = policy_evict_first();
+    unsigned long long* sched = g_cw_sched[p.slot];
 
+    // lane 0: the claim in progress (tiles [next, end)) and its cursor
+    long long next = 0, end = 0;
+    TileCursor ic;
+    auto issue_next = [&](int st) {   // claim the next tile, load it into stage st (lane 0)
+        if (next == end) {
+            const long long first = static_cast<long long>(atomicAdd(&sched[0], 1ull)) * kWClaim;
+            next = first;
+            end = first < p.n_tiles ? min(first + kWClaim, p.n_tiles) : first;
+            if (first < p.n_tiles) ic.init(p, first);
+        }
+        if (next < end) {
+            coords[st] = make_int4(ic.n, ic.by, ic.tb, 1);
+            w_issue_at<ELEM>(&tin, p, ic, wbase + st * Cfg::kStageBytes, &bars[st], pol);
+            ++next;
+            ic.advance(p);
+        } else {
+            coords[st] = make_int4(0, 0, 0, 0);
+        }
+    };
     if (lane == 0) {
-        for (int s = 0; s < kWStages; ++s) mbar_init(&bars[s], 1);
+        for (int st = 0; st < kWStages; ++st) mbar_init(&bars[st], 1);
         fence_mbar_init();
         prefetch_tmap(&tin);
         if (p.has_recon) prefetch_tmap(&tout);
-        TileCursor ic;
-        ic.init(p, t0);
-        for (int s = 0; s < kWStages - 1; ++s) {
-            if (t0 + s < t1) w_issue_at<ELEM>(&tin, p, ic, wbase + s * Cfg::kStageBytes, &bars[s], pol);
-            ic.advance(p);
-        }
+        for (int st = 0; st < kWStages - 1; ++st) issue_next(st);
     }
     __syncwarp();
 
@@ -231,14 +259,16 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
 
     unsigned long long acc = 0;
     int cur_n = -1;
-    int it = 0;
-    TileCursor cc, nc;   // the tile being consumed and the one kWStages - 1 ahead (next to issue)
-    cc.init(p, t0);
-    nc.init(p, t0 + kWStages - 1);
-    for (long long tix = t0; tix < t1; ++tix, ++it, cc.advance(p), nc.advance(p)) {
+    for (int it = 0;; ++it) {
         const int s = it % kWStages;
         uint8_t* stage = wbase + s * Cfg::kStageBytes;
+        const int4 cd = coords[s];
+        if (!cd.w) break;   // claims only grow: every later stage is empty too
         mbar_wait(&bars[s], (it / kWStages) & 1);
+        TileCursor cc;
+        cc.n = cd.x;
+        cc.by = cd.y;
+        cc.tb = cd.z;
         const int n = cc.n, by = cc.by, x0 = cc.x0();
         if (n != cur_n) {
 #pragma unroll
@@ -400,9 +430,7 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
                 bulk_commit();
                 bulk_wait_read<1>();   // the store of tile tix-1 has left the stage refilled next
             }
-            const long long nt = tix + kWStages - 1;
-            if (nt < t1) w_issue_at<ELEM>(&tin, p, nc, wbase + ((it + kWStages - 1) % kWStages) * Cfg::kStageBytes,
-                                       &bars[(it + kWStages - 1) % kWStages], pol);
+            issue_next((it + kWStages - 1) % kWStages);
         }
         __syncwarp();
     }
@@ -411,6 +439,11 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
     if (lane == 0) {
         if (acc) flush_sse(sse, p, cur_n, acc);
         if (p.has_recon) bulk_wait<0>();
+        if (atomicAdd(&sched[1], 1ull) == static_cast<unsigned long long>(p.total_warps) - 1) {
+            // every warp has claimed past the end: reset the slot for a later launch
+            sched[0] = 0;
+            sched[1] = 0;
+        }
     }
 }
 
@@ -475,10 +508,12 @@ int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon
         p.hi_c2 = static_cast<int>(static_cast<uint32_t>(p.hi_c) - ((p.magic_bits >> p.F) << p.hi_shift));
     }
     if (int e = smem_optin(reinterpret_cast<const void*>(codec_warp_kernel<ELEM, UNIFORM>), Cfg::kSmem)) return e;
-    long long warps = static_cast<long long>(num_sms()) * Cfg::kCtasPerSm * kWWarps;
-    if (warps > p.n_tiles) warps = p.n_tiles;
-    p.chunk = (p.n_tiles + warps - 1) / warps;
-    const long long grid = (warps + kWWarps - 1) / kWWarps;
+    long long grid = static_cast<long long>(num_sms()) * Cfg::kCtasPerSm;
+    const long long want = (p.n_tiles + kWWarps * kWClaim - 1) / (kWWarps * kWClaim);
+    if (want < grid) grid = want;
+    static std::atomic<unsigned> launch_seq{0};
+    p.slot = static_cast<int>(launch_seq.fetch_add(1) % kWSchedSlots);
+    p.total_warps = static_cast<int>(grid) * kWWarps;
     codec_warp_kernel<ELEM, UNIFORM><<<static_cast<unsigned>(grid), kWWarps * 32, Cfg::kSmem, st>>>(
         tin, tout, reinterpret_cast<unsigned long long*>(sse), p);
     return static_cast<int>(cudaGetLastError());
