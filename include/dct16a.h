@@ -155,6 +155,10 @@ DCT16A_API int dct16a_psnr(const void* ref, const void* test, const dct16a_desc*
  *           describes both src and recon; must not overlap src.
  *   sse   : uint64 out [batch] (exact; overwritten, not accumulated).
  *   psnr  : optional float64 out [batch] (may be NULL).
+ * Scheduling: the default kernels hand out tiles from one of 64 device-side
+ * counters per kernel, used round-robin by successive calls (as
+ * dct16a_forward); at most 64 dct16a_codec / dct16a_codec_allreduce launches
+ * may be executing at the same time (on any streams) per device.
  */
 DCT16A_API int dct16a_codec(const void* src, const dct16a_desc* desc,
                             const dct16a_quant* quant, void* recon,
