@@ -29,6 +29,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "16x16 2-D approx-DCT blocks/s and HBM GB/s (fraction of B200 peak), 1/2/4/8 GPUs"
+# best no-compute kernel for K1's 20/80 read/write byte mix on this box type (measured, round 1)
+MIX_CEILING_GBS = 6799.0
 N_IMG, H, W = 4096, 512, 512
 BLOCKS_PER_IMG = (H // 16) * (W // 16)
 BYTES_PER_BLOCK = 256 + 1024          # u8 block in + int32 block out
@@ -265,7 +267,12 @@ def run_ours(args):
                 "hbm_gbs": achieved,
                 "roofline": {"kernel": "fwd_kernel<1,5>", "bound": "hbm", "achieved": achieved, "peak": peak,
                              "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-                             "traffic": traffic, "alg_bytes_per_launch": alg_bytes},
+                             "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
+                             "note": "peak = copy burst (50/50 read/write); this kernel moves 20/80 "
+                                     "read/write, for which the best no-compute kernel measured "
+                                     f"{MIX_CEILING_GBS:.0f} GB/s (tools/mix_ceiling.cu, "
+                                     "profiles/r01_fwd_dynamic_sched.md)",
+                             "frac_of_mix_ceiling": achieved / MIX_CEILING_GBS},
                 "clocks": clk.summary(),
                 "e2e": {"value": e2e_value, "unit": "blocks/s", "h2d_bytes_per_step": N_IMG * H * W,
                         "d2h_bytes_per_step": nblocks * 1024, "steps": e2e_steps,
