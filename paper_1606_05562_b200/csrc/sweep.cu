@@ -14,7 +14,9 @@
 // codec_warp.cu): TMA tile ring in the 128-byte swizzle (tile128.cuh), row
 // pass, smem transposition, column pass (lane = column l) producing W ⊙ Z into
 // smem, then the sweep with lane = row i: N[i][:] += (W·Z_kl·T_ki)·T_l[:] in
-// float32 (exact: half-integers below 2^23, the +1152.5 rounding offset rides
+// float32 (exact: half-integers below 2^21 for 8-bit and 2^23 for 10-bit
+// input, the worst case over all blocks and all r pinned by tests/
+// test_exactness_bounds.py; the +1152.5 rounding offset rides
 // in N from the start; two columns per FFMA2; N is held as N·2^-35),
 // pixel = floor(N/2304) by one round-down multiply into the subnormal range
 // whose bits are the integer (8-bit; zonal_band.cu) or one round-down FMA onto

@@ -20,9 +20,10 @@
 //   Z in int16 (the K1 ranges).  W = 2304/(g_k g_l) on the zonal cells, the
 //   rounding offset 1152 on the DC input: every pixel of the inverse is N + 1152.
 // * Inverse in float32, exact, on N·2^-35: every input W·Z (+1152) and every
-//   partial sum is an integer of magnitude < 2^23 for 8-bit input (sum of W·|Z|
-//   over the band <= sqrt(sum W)·sqrt(2304·sum X²) < 7.1e6) times 2^-35, so every
-//   value is a normal float held exactly.  Lane (bp, l) runs the transposed
+//   value the transposed network forms is an integer of magnitude < 1.59e6
+//   (< 2^21) for 8-bit input and r <= 36 — the exact maximum of each value, a
+//   linear function of the block, over [0, 255]^256 (tests/
+//   test_exactness_bounds.py) — times 2^-35: a normal float held exactly.  Lane (bp, l) runs the transposed
 //   network down column l of both blocks (FADD2; inputs k <= BAND, the others
 //   compile-time zeros), the smem tile turns columns into rows, lane (bp, r8)
 //   runs rows r8, r8+8 of both blocks (inputs l <= BAND).
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
                 const int lo = uns ? static_cast<int>(z[k] & 0xFFFFu) : static_cast<int>(static_cast<int16_t>(z[k] & 0xFFFFu));
                 const uint32_t hs = z[k] - static_cast<uint32_t>(lo);   // Z_hi·2^16
                 const float hf = uns ? static_cast<float>(hs) : static_cast<float>(static_cast<int>(hs));
-                // exact in float: W·Z + 1152 and every later partial sum are integers below 2^23
+                // exact in float: W·Z + 1152 and every later value are integers below 2^21 (header)
                 c[k] = fma2(F2{make_float2(static_cast<float>(lo), hf)}, wl[k], k == 0 ? dc_off : F2{make_float2(0.0f, 0.0f)});
             }
             F2 u[16];

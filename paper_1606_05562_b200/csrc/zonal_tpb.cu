@@ -10,7 +10,8 @@
 // * Forward: the SWAR scheme of K1 (column pairs, PRMT transposition, row
 //   pairs), only rows k <= BAND.
 // * Inverse: float32 on the FMA pipe, exact: every value is a half-integer of
-//   magnitude < 2^22 (the DC input carries +1152.5 so the output is
+//   magnitude < 2^21 (tests/test_exactness_bounds.py; the DC input carries
+//   +1152.5 so the output is
 //   N + 1152.5, and pixel = floor((N + 1152.5)/2304) = round_half_away(N/2304)).
 //   One round-down FMA a·fl(1/2304) + 2^23 gives the floor: the product errs by
 //   < 2^-24·t, below the 1/4608 distance of (N + 1152.5)/2304 (an odd multiple
