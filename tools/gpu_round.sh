@@ -6,7 +6,7 @@ nvidia-smi > gpurun_out/nvsmi.txt 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
-timeout 900 python tools/bench_configs.py --configs 1,3,4 > gpurun_out/configs.jsonl 2> gpurun_out/configs.err; echo "cfg rc=$?"
+timeout 900 python tools/bench_configs.py --configs 1,3,4,5 > gpurun_out/configs.jsonl 2> gpurun_out/configs.err; echo "cfg rc=$?"
 timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
    python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu.log 2>&1; echo "ncu rc=$?"
