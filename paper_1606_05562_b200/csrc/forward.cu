@@ -4,8 +4,9 @@
 //
 // B200 design:
 //  * one thread owns one 16x16 block; a warp owns a tile of 32 horizontally
-//    adjacent blocks of one 16-row strip; warps are persistent and walk tiles
-//    with a stride of the total warp count;
+//    adjacent blocks of one 16-row strip; warps are persistent and claim
+//    tiles in increasing order from a global counter (dynamic scheduler
+//    below), so the tiles in flight form one compact address window;
 //  * TMA (cp.async.bulk.tensor) streams the 16-row strip tile into a 2-stage
 //    per-warp smem ring (mbarrier complete_tx); pixels are read back with
 //    128-bit ld.shared (conflict-free: a phase of 8 lanes reads 128 contiguous
@@ -19,8 +20,9 @@
 //    the row pass then yields two rows of Z per network (8-bit: Z_00 in
 //    [0, 65280] is the only entry outside int16 and is decoded unsigned);
 //  * each Z row pair (128 B per block) is staged in smem in the TMA 128-byte
-//    swizzle (conflict-free STS) and written by one TMA tensor store of
-//    32 blocks x 128 B; two staging buffers alternate (bulk async-groups).
+//    swizzle (conflict-free STS); by default (store mode 5) the whole 32 KB
+//    tile leaves in one TMA tensor store (bulk async-group), the other modes
+//    below store 4-16 KB pieces from alternating buffers.
 #include <cuda.h>
 #include <stdint.h>
 #include <stdlib.h>
