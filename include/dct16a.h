@@ -92,7 +92,8 @@ typedef struct dct16a_quant {
  * Scheduling: the kernel hands out tiles from one of 64 device-side counters
  * used round-robin by successive calls (a compact write window);
  * at most 64 dct16a_forward / dct16a_forward16 launches may be executing at
- * the same time (on any streams) per device.
+ * the same time (on any streams) per device.  A launch captured in a CUDA
+ * graph keeps its counter: replays of one graph must not overlap in time.
  */
 DCT16A_API int dct16a_forward(const void* src, const dct16a_desc* desc,
                               int32_t* coef, void* stream);
@@ -158,7 +159,8 @@ DCT16A_API int dct16a_psnr(const void* ref, const void* test, const dct16a_desc*
  * Scheduling: the default kernels hand out tiles from one of 64 device-side
  * counters per kernel, used round-robin by successive calls (as
  * dct16a_forward); at most 64 dct16a_codec / dct16a_codec_allreduce launches
- * may be executing at the same time (on any streams) per device.
+ * may be executing at the same time (on any streams) per device, and replays
+ * of one captured CUDA graph must not overlap in time.
  */
 DCT16A_API int dct16a_codec(const void* src, const dct16a_desc* desc,
                             const dct16a_quant* quant, void* recon,
