@@ -41,6 +41,7 @@
 #include <math.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <type_traits>
 
@@ -96,7 +97,7 @@ __device__ unsigned long long g_cw_sched[kWSchedSlots][2];
 struct WParams {
     int W, BX, BY, VH, tiles_per_strip, maxpix;
     long long n_tiles;
-    int slot, total_warps;
+    int slot, total_warps, claim;   // dynamic tile scheduler (claim = tiles per claim)
     int has_recon;
     // fused SSE all-reduce (dct16a_codec_allreduce): every image's SSE is added
     // into sse_peers[q][frame_offset + n] of every peer q; n_peers = 0: local sse
@@ -203,9 +204,9 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
     TileCursor ic;
     auto issue_next = [&](int st) {   // claim the next tile, load it into stage st (lane 0)
         if (next == end) {
-            const long long first = static_cast<long long>(atomicAdd(&sched[0], 1ull)) * kWClaim;
+            const long long first = static_cast<long long>(atomicAdd(&sched[0], 1ull)) * p.claim;
             next = first;
-            end = first < p.n_tiles ? min(first + kWClaim, p.n_tiles) : first;
+            end = first < p.n_tiles ? min(first + p.claim, p.n_tiles) : first;
             if (first < p.n_tiles) ic.init(p, first);
         }
         if (next < end) {
@@ -509,7 +510,10 @@ int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon
     }
     if (int e = smem_optin(reinterpret_cast<const void*>(codec_warp_kernel<ELEM, UNIFORM>), Cfg::kSmem)) return e;
     long long grid = static_cast<long long>(num_sms()) * Cfg::kCtasPerSm;
-    const long long want = (p.n_tiles + kWWarps * kWClaim - 1) / (kWWarps * kWClaim);
+    // runs of up to kWClaim tiles, shorter when there are few tiles per resident warp
+    // (a small batch then still spreads over many warps)
+    p.claim = static_cast<int>(std::min<long long>(kWClaim, std::max<long long>(1, p.n_tiles / (grid * kWWarps * 4))));
+    const long long want = (p.n_tiles + kWWarps * p.claim - 1) / (kWWarps * p.claim);
     if (want < grid) grid = want;
     static std::atomic<unsigned> launch_seq{0};
     p.slot = static_cast<int>(launch_seq.fetch_add(1) % kWSchedSlots);

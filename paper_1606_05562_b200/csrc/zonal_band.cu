@@ -39,6 +39,7 @@
 #include <cuda.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <atomic>
 
 #include "internal.h"
@@ -93,7 +94,7 @@ struct BParams {
     long long n_tiles;
     int r;
     int has_recon;
-    int slot, total_warps;   // dynamic tile scheduler
+    int slot, total_warps, claim;   // dynamic tile scheduler (claim = tiles per claim)
 };
 
 // Dynamic tile scheduler (as the forward kernel's, forward.cu): warps claim runs
@@ -130,9 +131,9 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
     // claim the next tile and issue its load into stage `st` (lane 0 only)
     auto issue_next = [&](int st) {
         if (next == end) {
-            const long long first = static_cast<long long>(atomicAdd(&sched[0], 1ull)) * kBClaim;
+            const long long first = static_cast<long long>(atomicAdd(&sched[0], 1ull)) * p.claim;
             next = first;
-            end = first < p.n_tiles ? min(first + kBClaim, p.n_tiles) : first;
+            end = first < p.n_tiles ? min(first + p.claim, p.n_tiles) : first;
             if (first < p.n_tiles) ic.init(p, first);
         }
         if (next < end) {
@@ -348,7 +349,10 @@ int launch_zb(const void* src, const Geom& g, int r, void* recon, uint64_t* sse,
     p.has_recon = recon != nullptr;
     if (int e = smem_optin(reinterpret_cast<const void*>(zband_kernel<BAND>), kBSmem)) return e;
     long long grid = static_cast<long long>(num_sms()) * DCT16A_ZB_CTAS;
-    const long long want = (p.n_tiles + kBWarps * kBClaim - 1) / (kBWarps * kBClaim);
+    // runs of up to kBClaim tiles, shorter when there are few tiles per resident warp
+    // (a small batch then still spreads over many warps)
+    p.claim = static_cast<int>(std::min<long long>(kBClaim, std::max<long long>(1, p.n_tiles / (grid * kBWarps * 4))));
+    const long long want = (p.n_tiles + kBWarps * p.claim - 1) / (kBWarps * p.claim);
     if (want < grid) grid = want;
     static std::atomic<unsigned> launch_seq{0};
     p.slot = static_cast<int>(launch_seq.fetch_add(1) % kBSchedSlots);
