@@ -26,31 +26,47 @@
 namespace dct16a {
 
 // ------------------------------------------------------------------ K4
-__global__ void quantize_kernel(const int4* __restrict__ coef, int4* __restrict__ qcoef,
-                                float4* __restrict__ scaled, long long n4, int mode, int r, int step) {
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int4 z = coef[i];
-        const int pos = static_cast<int>((i * 4) & 255);
-        const int k = pos >> 4, l0 = pos & 15;
-        const int zz[4] = {z.x, z.y, z.z, z.w};
-        int qq[4];
-        float ss[4];
+// Elementwise over int4 groups of coefficients.  The grid stride is a multiple
+// of 64 int4 (one 16x16 block), so every thread always sees the same four
+// cells (k, l0..l0+3): their zig-zag mask, scale s_k·s_l and exact-decision
+// constants are computed once per thread.  Streaming loads/stores (.cs).
+__global__ void __launch_bounds__(256) quantize_kernel(const int4* __restrict__ coef, int4* __restrict__ qcoef,
+                                                       float4* __restrict__ scaled, long long n4, int mode, int r,
+                                                       int step) {
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;   // multiple of 64
+    long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    const int pos = static_cast<int>((i * 4) & 255);
+    const int k = pos >> 4, l0 = pos & 15;
+    float sc[4], cq[4];
+    uint64_t d2g[4];
+    bool keep[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int l = l0 + e;
-            const double s = s_of(k) * s_of(l);
-            if (mode == DCT16A_ZONAL) {
-                qq[e] = zigzag_rank(k, l) < r ? zz[e] : 0;
-                ss[e] = static_cast<float>(s * static_cast<double>(qq[e]));
-            } else {
-                const uint64_t d2g = static_cast<uint64_t>(step) * step * (g_of(k) * g_of(l));
-                qq[e] = uniform_level(zz[e], static_cast<float>(s / step), d2g);
-                ss[e] = static_cast<float>(s * static_cast<double>(zz[e]));
-            }
+    for (int e = 0; e < 4; ++e) {
+        const int l = l0 + e;
+        const double s = s_of(k) * s_of(l);
+        sc[e] = static_cast<float>(s);
+        cq[e] = static_cast<float>(s / step);
+        d2g[e] = static_cast<uint64_t>(step) * step * (g_of(k) * g_of(l));
+        keep[e] = zigzag_rank(k, l) < r;
+    }
+    if (mode == DCT16A_ZONAL) {
+        for (; i < n4; i += stride) {
+            const int4 z = __ldcs(coef + i);
+            const int q0 = keep[0] ? z.x : 0, q1 = keep[1] ? z.y : 0, q2 = keep[2] ? z.z : 0, q3 = keep[3] ? z.w : 0;
+            __stcs(qcoef + i, make_int4(q0, q1, q2, q3));
+            if (scaled)
+                __stcs(scaled + i, make_float4(sc[0] * static_cast<float>(q0), sc[1] * static_cast<float>(q1),
+                                               sc[2] * static_cast<float>(q2), sc[3] * static_cast<float>(q3)));
         }
-        qcoef[i] = make_int4(qq[0], qq[1], qq[2], qq[3]);
-        if (scaled) scaled[i] = make_float4(ss[0], ss[1], ss[2], ss[3]);
+    } else {
+        for (; i < n4; i += stride) {
+            const int4 z = __ldcs(coef + i);
+            __stcs(qcoef + i, make_int4(uniform_level(z.x, cq[0], d2g[0]), uniform_level(z.y, cq[1], d2g[1]),
+                                        uniform_level(z.z, cq[2], d2g[2]), uniform_level(z.w, cq[3], d2g[3])));
+            if (scaled)
+                __stcs(scaled + i, make_float4(sc[0] * static_cast<float>(z.x), sc[1] * static_cast<float>(z.y),
+                                               sc[2] * static_cast<float>(z.z), sc[3] * static_cast<float>(z.w)));
+        }
     }
 }
 
@@ -105,63 +121,83 @@ constexpr int kBlkPerCta = 8;   // standalone inverse: 16 threads per block
 }  // namespace
 
 // ------------------------------------------------------------------ K5
+// 16 threads per block (thread t: column t, then row t), 8 blocks per CTA,
+// persistent CTAs walking groups of 8 blocks, per-thread constants of column t
+// computed once.  Zonal: exact int32 networks (any int32 levels with |N| < 2^31);
+// uniform: float64 with the exact decision near .5 (reading A10).
 template <bool UNIFORM>
 __global__ void __launch_bounds__(128) inverse_kernel(const int32_t* __restrict__ qcoef, uint8_t* recon,
                                                       const Geom g, int step) {
     using V = typename std::conditional<UNIFORM, double, int32_t>::type;
     __shared__ V sm[kBlkPerCta][16][17];
     const int sub = threadIdx.x >> 4, t = threadIdx.x & 15;
-    const long long b = static_cast<long long>(blockIdx.x) * kBlkPerCta + sub;
-    const bool valid = b < g.nblocks;
-    if (valid) {
-        // column t of the level block, weighted: c_k = weight(k, t)·qcoef[k][t]
-        V c[16], u[16];
-        const int32_t* blk = qcoef + b * 256;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            const int32_t q = blk[k * 16 + t];
-            if constexpr (UNIFORM) c[k] = static_cast<double>(step) * static_cast<double>(q) * (s_of(k) * s_of(t));
-            else c[k] = q * w_of(k, t);
-        }
-        net_inv(c, u);   // Tᵀ applied down the column
-#pragma unroll
-        for (int i = 0; i < 16; ++i) sm[sub][i][t] = u[i];
-    }
-    __syncthreads();
-    if (!valid) return;
-    V rrow[16], a[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) rrow[j] = sm[sub][t][j];
-    net_inv(rrow, a);    // ... and along row t: A′ = Tᵀ·B̂·T
     const int maxpix = (1 << g.bits) - 1;
-    int pix[16];
-    if constexpr (UNIFORM) {
-        // floor(A′ + 1/2) from the float64 value; pixels within 2^-20 of a .5
-        // boundary are decided exactly from the levels (uexact.cuh, reading A10)
-        uint32_t nm = 0;
-        int n0[16];
+    // column t constants: zonal W = 2304/(g_k·g_t); uniform Δ·s_k·s_t by class of k
+    int32_t wcol[16];
+    double wq[3];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            bool nr;
-            pix[j] = round_f64(a[j], nr, n0[j]);
-            nm |= (nr ? 1u : 0u) << j;
+    for (int k = 0; k < 16; ++k) wcol[k] = w_of(k, t);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) wq[c] = static_cast<double>(step) * s_of(c == 0 ? 0 : (c == 1 ? 2 : 3)) * s_of(t);
+    const long long stride = static_cast<long long>(gridDim.x) * kBlkPerCta;
+    for (long long b0 = static_cast<long long>(blockIdx.x) * kBlkPerCta; b0 < g.nblocks; b0 += stride) {
+        const long long b = b0 + sub;
+        const bool valid = b < g.nblocks;
+        if (valid) {
+            // column t of the level block, weighted: c_k = weight(k, t)·qcoef[k][t]
+            V c[16], u[16];
+            const int32_t* blk = qcoef + b * 256;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const int32_t q = __ldcs(blk + k * 16 + t);
+                if constexpr (UNIFORM) {
+                    const int gk = g_of(k);
+                    c[k] = __int2double_rn(q) * wq[gk == 16 ? 0 : (gk == 12 ? 1 : 2)];
+                } else {
+                    c[k] = q * wcol[k];
+                }
+            }
+            net_inv(c, u);   // Tᵀ applied down the column
+#pragma unroll
+            for (int i = 0; i < 16; ++i) sm[sub][i][t] = u[i];
         }
-        if (nm) {
-            int32_t qb[256];
-            for (int i = 0; i < 256; ++i) qb[i] = qcoef[b * 256 + i];
+        __syncthreads();
+        if (valid) {
+            V rrow[16], a[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if ((nm >> j) & 1u) pix[j] = uniform_exact_floor(qb, t, j, step, n0[j]);
+            for (int j = 0; j < 16; ++j) rrow[j] = sm[sub][t][j];
+            net_inv(rrow, a);   // ... and along row t: A′ = Tᵀ·B̂·T
+            int pix[16];
+            if constexpr (UNIFORM) {
+                // floor(A′ + 1/2) from the float64 value; pixels within 2^-20 of a .5
+                // boundary are decided exactly from the levels (uexact.cuh, reading A10)
+                uint32_t nm = 0;
+                int n0[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    bool nr;
+                    pix[j] = round_f64(a[j], nr, n0[j]);
+                    nm |= (nr ? 1u : 0u) << j;
+                }
+                if (nm) {
+                    int32_t qb[256];
+                    for (int i = 0; i < 256; ++i) qb[i] = qcoef[b * 256 + i];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if ((nm >> j) & 1u) pix[j] = uniform_exact_floor(qb, t, j, step, n0[j]);
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) pix[j] = min(max(pix[j], 0), maxpix);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) pix[j] = zonal_pixel(a[j], maxpix);
+            }
+            int n, row0;
+            const long long off = block_offset(b, g, &n, &row0);
+            store_row(recon + off + static_cast<long long>(t) * g.pitch, g.elem, pix);
         }
-#pragma unroll
-        for (int j = 0; j < 16; ++j) pix[j] = min(max(pix[j], 0), maxpix);
-    } else {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) pix[j] = zonal_pixel(a[j], maxpix);
+        __syncthreads();   // sm is rewritten by the next group
     }
-    int n, row0;
-    const long long off = block_offset(b, g, &n, &row0);
-    store_row(recon + off + static_cast<long long>(t) * g.pitch, g.elem, pix);
 }
 
 // ------------------------------------------------------- fused codec (K2/K3)
@@ -361,7 +397,9 @@ int launch_quantize(const int32_t* coef, const Geom& g, const dct16a_quant& q, i
 }
 
 int launch_inverse(const int32_t* qcoef, const Geom& g, const dct16a_quant& q, void* recon, cudaStream_t st) {
-    const long long grid = (g.nblocks + kBlkPerCta - 1) / kBlkPerCta;
+    long long grid = (g.nblocks + kBlkPerCta - 1) / kBlkPerCta;
+    const long long cap = static_cast<long long>(num_sms()) * (q.mode == DCT16A_UNIFORM ? 4 : 8);
+    if (grid > cap) grid = cap;
     if (q.mode == DCT16A_UNIFORM)
         inverse_kernel<true><<<static_cast<unsigned>(grid), 128, 0, st>>>(qcoef, static_cast<uint8_t*>(recon), g, q.step);
     else
