@@ -5,7 +5,7 @@
 // (one box for uint8, two for uint16), so that the 8 lanes of a quarter-warp
 // reading rows 0-7 of one block hit 8 distinct 16-byte chunks.  Every stage
 // base must be 1024-byte aligned (the swizzle takes smem address bits 7-9).
-// P is any parameter struct with fields W, BY and tiles_per_strip.
+// P is any parameter struct with fields W, BY, tiles_per_strip and n_tiles.
 #pragma once
 #include <cuda.h>
 #include <stdint.h>
@@ -38,6 +38,14 @@ struct TileCursor {
     int n, by, tb;
     template <class P>
     __device__ __forceinline__ void init(const P& p, long long tix) {
+        if (p.n_tiles <= 0x7FFFFFFFLL) {   // 32-bit divisions (the common case)
+            const uint32_t t = static_cast<uint32_t>(tix);
+            const uint32_t strip = t / static_cast<uint32_t>(p.tiles_per_strip);
+            tb = static_cast<int>(t - strip * static_cast<uint32_t>(p.tiles_per_strip));
+            n = static_cast<int>(strip / static_cast<uint32_t>(p.BY));
+            by = static_cast<int>(strip - static_cast<uint32_t>(n) * static_cast<uint32_t>(p.BY));
+            return;
+        }
         int x0;
         w_tile_coords<1>(p, tix, &n, &by, &x0);
         tb = x0 / (kWTile * 16);
