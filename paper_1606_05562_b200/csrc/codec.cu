@@ -19,6 +19,7 @@
 
 #include "internal.h"
 #include "net16.cuh"
+#include "ptx.cuh"
 #include "quant.cuh"
 #include "tables.cuh"
 #include "uexact.cuh"
@@ -116,21 +117,30 @@ __device__ __forceinline__ long long block_offset(long long b, const Geom& g, in
     return n * g.istride + static_cast<long long>(by * 16) * g.pitch + bx * 16LL * g.elem;
 }
 
-constexpr int kBlkPerCta = 8;   // standalone inverse: 16 threads per block
-
 }  // namespace
 
 // ------------------------------------------------------------------ K5
-// 16 threads per block (thread t: column t, then row t), 8 blocks per CTA,
-// persistent CTAs walking groups of 8 blocks, per-thread constants of column t
-// computed once.  Zonal: exact int32 networks (any int32 levels with |N| < 2^31);
-// uniform: float64 with the exact decision near .5 (reading A10).
+// 16 threads per block (thread t: column t, then row t); each warp owns a pair
+// of consecutive blocks (2 KB of block-major levels) and works independently:
+// its lane 0 streams the warp's next pair into the second of two per-warp smem
+// buffers by bulk copies (one per block, slots 16 words apart so the two
+// blocks of the warp read different banks) while the current pair computes;
+// the in-block transposition is a per-warp smem tile (no CTA barrier).
+// Per-thread column constants are computed once.  Zonal: exact int32 networks
+// (any int32 levels with |N| < 2^31); uniform: float64 with the exact decision
+// near .5 (reading A10).
+constexpr int kInvWarps = 4;
+constexpr int kInvSlot = 256 + 16;   // words per block slot in a level buffer
+
 template <bool UNIFORM>
-__global__ void __launch_bounds__(128) inverse_kernel(const int32_t* __restrict__ qcoef, uint8_t* recon,
-                                                      const Geom g, int step) {
+__global__ void __launch_bounds__(kInvWarps * 32) inverse_kernel(const int32_t* __restrict__ qcoef, uint8_t* recon,
+                                                                 const Geom g, int step) {
     using V = typename std::conditional<UNIFORM, double, int32_t>::type;
-    __shared__ V sm[kBlkPerCta][16][17];
-    const int sub = threadIdx.x >> 4, t = threadIdx.x & 15;
+    __shared__ V sm[kInvWarps][2][16][17];
+    __shared__ __align__(16) int32_t lv[kInvWarps][2][2 * kInvSlot];
+    __shared__ __align__(8) uint64_t bars[kInvWarps][2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int h = lane >> 4, t = lane & 15;
     const int maxpix = (1 << g.bits) - 1;
     // column t constants: zonal W = 2304/(g_k·g_t); uniform Δ·s_k·s_t by class of k
     int32_t wcol[16];
@@ -139,17 +149,38 @@ __global__ void __launch_bounds__(128) inverse_kernel(const int32_t* __restrict_
     for (int k = 0; k < 16; ++k) wcol[k] = w_of(k, t);
 #pragma unroll
     for (int c = 0; c < 3; ++c) wq[c] = static_cast<double>(step) * s_of(c == 0 ? 0 : (c == 1 ? 2 : 3)) * s_of(t);
-    const long long stride = static_cast<long long>(gridDim.x) * kBlkPerCta;
-    for (long long b0 = static_cast<long long>(blockIdx.x) * kBlkPerCta; b0 < g.nblocks; b0 += stride) {
-        const long long b = b0 + sub;
+    const long long npairs = (g.nblocks + 1) / 2;
+    const long long stride = static_cast<long long>(gridDim.x) * kInvWarps;
+    long long pr = static_cast<long long>(blockIdx.x) * kInvWarps + warp;
+    uint64_t* bar = bars[warp];
+    auto issue = [&](long long pp, int buf) {   // lane 0: the levels of block pair pp
+        const int nv = static_cast<int>(min(2LL, g.nblocks - 2 * pp));
+        fence_async_smem();   // this warp's generic reads of the buffer (ordered by __syncwarp) precede the copy
+        mbar_arrive_expect_tx(&bar[buf], static_cast<uint32_t>(nv * 1024));
+        for (int i = 0; i < nv; ++i) bulk_load(&lv[warp][buf][i * kInvSlot], qcoef + (2 * pp + i) * 256, 1024u, &bar[buf]);
+    };
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        if (pr < npairs) issue(pr, 0);
+    }
+    __syncwarp();
+    for (int it = 0; pr < npairs; pr += stride, ++it) {
+        const int buf = it & 1;
+        // the other buffer was last read in iteration it-1, closed by its final __syncwarp
+        if (lane == 0 && pr + stride < npairs) issue(pr + stride, buf ^ 1);
+        mbar_wait(&bar[buf], (it >> 1) & 1);
+        const long long b = 2 * pr + h;
         const bool valid = b < g.nblocks;
+        const int32_t* blk = &lv[warp][buf][h * kInvSlot];
+        V (*tile)[17] = sm[warp][h];
         if (valid) {
             // column t of the level block, weighted: c_k = weight(k, t)·qcoef[k][t]
             V c[16], u[16];
-            const int32_t* blk = qcoef + b * 256;
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
-                const int32_t q = __ldcs(blk + k * 16 + t);
+                const int32_t q = blk[k * 16 + t];
                 if constexpr (UNIFORM) {
                     const int gk = g_of(k);
                     c[k] = __int2double_rn(q) * wq[gk == 16 ? 0 : (gk == 12 ? 1 : 2)];
@@ -159,13 +190,13 @@ __global__ void __launch_bounds__(128) inverse_kernel(const int32_t* __restrict_
             }
             net_inv(c, u);   // Tᵀ applied down the column
 #pragma unroll
-            for (int i = 0; i < 16; ++i) sm[sub][i][t] = u[i];
+            for (int i = 0; i < 16; ++i) tile[i][t] = u[i];
         }
-        __syncthreads();
+        __syncwarp();
         if (valid) {
             V rrow[16], a[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) rrow[j] = sm[sub][t][j];
+            for (int j = 0; j < 16; ++j) rrow[j] = tile[t][j];
             net_inv(rrow, a);   // ... and along row t: A′ = Tᵀ·B̂·T
             int pix[16];
             if constexpr (UNIFORM) {
@@ -181,7 +212,7 @@ __global__ void __launch_bounds__(128) inverse_kernel(const int32_t* __restrict_
                 }
                 if (nm) {
                     int32_t qb[256];
-                    for (int i = 0; i < 256; ++i) qb[i] = qcoef[b * 256 + i];
+                    for (int i = 0; i < 256; ++i) qb[i] = blk[i];
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
                         if ((nm >> j) & 1u) pix[j] = uniform_exact_floor(qb, t, j, step, n0[j]);
@@ -196,7 +227,7 @@ __global__ void __launch_bounds__(128) inverse_kernel(const int32_t* __restrict_
             const long long off = block_offset(b, g, &n, &row0);
             store_row(recon + off + static_cast<long long>(t) * g.pitch, g.elem, pix);
         }
-        __syncthreads();   // sm is rewritten by the next group
+        __syncwarp();   // the tile and lv[buf] are rewritten later
     }
 }
 
@@ -397,13 +428,14 @@ int launch_quantize(const int32_t* coef, const Geom& g, const dct16a_quant& q, i
 }
 
 int launch_inverse(const int32_t* qcoef, const Geom& g, const dct16a_quant& q, void* recon, cudaStream_t st) {
-    long long grid = (g.nblocks + kBlkPerCta - 1) / kBlkPerCta;
+    const long long npairs = (g.nblocks + 1) / 2;
+    long long grid = (npairs + kInvWarps - 1) / kInvWarps;
     const long long cap = static_cast<long long>(num_sms()) * (q.mode == DCT16A_UNIFORM ? 4 : 8);
     if (grid > cap) grid = cap;
     if (q.mode == DCT16A_UNIFORM)
-        inverse_kernel<true><<<static_cast<unsigned>(grid), 128, 0, st>>>(qcoef, static_cast<uint8_t*>(recon), g, q.step);
+        inverse_kernel<true><<<static_cast<unsigned>(grid), kInvWarps * 32, 0, st>>>(qcoef, static_cast<uint8_t*>(recon), g, q.step);
     else
-        inverse_kernel<false><<<static_cast<unsigned>(grid), 128, 0, st>>>(qcoef, static_cast<uint8_t*>(recon), g, q.step);
+        inverse_kernel<false><<<static_cast<unsigned>(grid), kInvWarps * 32, 0, st>>>(qcoef, static_cast<uint8_t*>(recon), g, q.step);
     return static_cast<int>(cudaGetLastError());
 }
 
