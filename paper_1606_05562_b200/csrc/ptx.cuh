@@ -58,6 +58,19 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// Two float32 products rounded toward -inf, subnormal results KEPT (no .ftz,
+// whatever the compile flags): the zonal kernels read the pixel integer from
+// the bit pattern of a subnormal product (zonal_band.cu header).
+__device__ __forceinline__ float2 fmul2_rd_keep_subnormal(float2 a, float2 b) {
+    unsigned long long ua, ub, ud;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ua) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ub) : "f"(b.x), "f"(b.y));
+    asm("mul.rm.f32x2 %0, %1, %2;" : "=l"(ud) : "l"(ua), "l"(ub));
+    float2 d;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(ud));
+    return d;
+}
+
 // Bulk (non-tensor) copy global -> smem, completion signalled on `bar`
 // (bytes a multiple of 16, both addresses 16-byte aligned).
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
                     for (int q = 0; q < 4; ++q) {
                         // (N·2^-35)·fl(2^-114/2304) rounded down to the subnormal grid:
                         // the bits are floor(N·fl(1/2304)) (negative -> sign bit -> 0)
-                        const float2 f0 = __fmul2_rd(N[2 * q], pix2), f1 = __fmul2_rd(N[2 * q + 1], pix2);
+                        const float2 f0 = fmul2_rd_keep_subnormal(N[2 * q], pix2), f1 = fmul2_rd_keep_subnormal(N[2 * q + 1], pix2);
                         const int v[4] = {__float_as_int(f0.x), __float_as_int(f0.y), __float_as_int(f1.x),
                                           __float_as_int(f1.y)};
                         const uint32_t pk = pack2_sat_u8(v[1], v[0], pack2_sat_u8(v[3], v[2], 0u));

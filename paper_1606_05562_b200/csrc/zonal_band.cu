@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
             for (int j = 0; j < 16; ++j) {
                 // floor((N + 1152)/2304) for both blocks by one round-down multiply into
                 // the subnormal range: the bits of the result are the integer itself
-                const float2 r = __fmul2_rd(a[j].v, pix_scale.v);
+                const float2 r = fmul2_rd_keep_subnormal(a[j].v, pix_scale.v);
                 pa[j] = __float_as_int(r.x);
                 pb[j] = __float_as_int(r.y);
             }

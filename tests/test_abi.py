@@ -171,3 +171,14 @@ def test_codec_allreduce_validation():
     assert f(buf, ctypes.byref(d), ctypes.byref(q), None, None, 2, 0, None) == -1
     bad = (ctypes.c_void_p * 1)(ctypes.c_void_p((1 << 20) + 4))
     assert f(buf, ctypes.byref(d), ctypes.byref(q), None, bad, 1, 0, None) == -4
+
+
+def test_build_flags_keep_subnormals():
+    """The zonal kernels read pixel integers from subnormal float products (and
+    state it explicitly with PTX mul.rm.f32x2 without .ftz); the library build
+    must not switch on flush-to-zero or fast math globally either."""
+    from paper_1606_05562_b200 import build
+    flags = " ".join(build.FLAGS)
+    assert "fast_math" not in flags and "ftz=true" not in flags
+    src = open(os.path.join(ROOT, "paper_1606_05562_b200", "csrc", "ptx.cuh")).read()
+    assert "mul.rm.f32x2" in src and "mul.rm.ftz" not in src
