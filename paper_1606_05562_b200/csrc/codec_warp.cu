@@ -93,6 +93,8 @@ constexpr int kWClaim = DCT16A_CW_CLAIM;   // consecutive tiles per claim
 // reset by the last warp (at most 64 concurrent launches per device).
 constexpr int kWSchedSlots = 64;
 __device__ unsigned long long g_cw_sched[kWSchedSlots][2];
+// one host-side slot counter for every instantiation of the kernel (they share g_cw_sched)
+std::atomic<unsigned> g_cw_launch_seq{0};
 
 struct WParams {
     int W, BX, BY, VH, tiles_per_strip, maxpix;
@@ -515,8 +517,7 @@ int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon
     p.claim = static_cast<int>(std::min<long long>(kWClaim, std::max<long long>(1, p.n_tiles / (grid * kWWarps * 4))));
     const long long want = (p.n_tiles + kWWarps * p.claim - 1) / (kWWarps * p.claim);
     if (want < grid) grid = want;
-    static std::atomic<unsigned> launch_seq{0};
-    p.slot = static_cast<int>(launch_seq.fetch_add(1) % kWSchedSlots);
+    p.slot = static_cast<int>(g_cw_launch_seq.fetch_add(1) % kWSchedSlots);
     p.total_warps = static_cast<int>(grid) * kWWarps;
     codec_warp_kernel<ELEM, UNIFORM><<<static_cast<unsigned>(grid), kWWarps * 32, Cfg::kSmem, st>>>(
         tin, tout, reinterpret_cast<unsigned long long*>(sse), p);

@@ -88,6 +88,8 @@ struct FwdParams {
 // launches; the last warp of a launch resets its slot.
 constexpr int kSchedSlots = 64;
 __device__ unsigned long long g_fwd_sched[kSchedSlots][2];
+// one host-side slot counter for every instantiation of the kernel (they share g_fwd_sched)
+std::atomic<unsigned> g_fwd_launch_seq{0};
 
 // Pad the dynamic smem base to 1024 B (128-byte swizzle atoms) while keeping
 // the pointer derived from the __shared__ array, so the compiler emits LDS/STS.
@@ -381,8 +383,7 @@ int launch_fwd_t(const void* src, const Geom& g, int32_t* coef, cudaStream_t st)
     const long long want = (p.n_tiles + Cfg::kWarps - 1) / Cfg::kWarps;
     long long grid = static_cast<long long>(num_sms()) * Cfg::kMinCtas;
     if (want < grid) grid = want;
-    static std::atomic<unsigned> launch_seq{0};
-    p.slot = static_cast<int>(launch_seq.fetch_add(1) % kSchedSlots);
+    p.slot = static_cast<int>(g_fwd_launch_seq.fetch_add(1) % kSchedSlots);
     p.total_warps = static_cast<int>(grid) * Cfg::kWarps;
     fwd_kernel<ELEM, SM><<<static_cast<unsigned>(grid), Cfg::kWarps * 32, Cfg::kSmem, st>>>(tin, tout, coef, p);
     return static_cast<int>(cudaGetLastError());

@@ -104,6 +104,8 @@ struct BParams {
 // slot (at most 64 concurrent launches per device).
 constexpr int kBSchedSlots = 64;
 __device__ unsigned long long g_zb_sched[kBSchedSlots][2];
+// one host-side slot counter for every instantiation of the kernel (they share g_zb_sched)
+std::atomic<unsigned> g_zb_launch_seq{0};
 
 }  // namespace
 
@@ -354,8 +356,7 @@ int launch_zb(const void* src, const Geom& g, int r, void* recon, uint64_t* sse,
     p.claim = static_cast<int>(std::min<long long>(kBClaim, std::max<long long>(1, p.n_tiles / (grid * kBWarps * 4))));
     const long long want = (p.n_tiles + kBWarps * p.claim - 1) / (kBWarps * p.claim);
     if (want < grid) grid = want;
-    static std::atomic<unsigned> launch_seq{0};
-    p.slot = static_cast<int>(launch_seq.fetch_add(1) % kBSchedSlots);
+    p.slot = static_cast<int>(g_zb_launch_seq.fetch_add(1) % kBSchedSlots);
     p.total_warps = static_cast<int>(grid) * kBWarps;
     zband_kernel<BAND><<<static_cast<unsigned>(grid), kBWarps * 32, kBSmem, st>>>(
         tin, tout, reinterpret_cast<unsigned long long*>(sse), p);

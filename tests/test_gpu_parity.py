@@ -725,6 +725,50 @@ def test_codec_concurrent_streams(codec_path):
         assert sses[0].cpu().tolist() == refs[mode][0]["sse"]
 
 
+def test_mixed_kernels_concurrent_streams():
+    """Different instantiations of the scheduled kernels in flight at once (they
+    share one counter array per kernel family): 8-bit int32 forward, 16-bit
+    forward, 10-bit forward, zonal codec on bands 3/5/7, uniform codec on 8 and
+    10 bits, each on its own stream, three rounds; every result equals the oracle."""
+    u8 = synth.batch_u8(range(300, 303), 64, 384)
+    u10 = (synth.batch_u8(range(310, 312), 64, 256).astype(np.int16) * 4 + 3).astype(np.int16)
+    x8, x10 = to_dev(u8), to_dev(u10)
+    z8, z10 = oracle_Z(u8), oracle_Z(u10)
+    codec_cases = [(x8, u8, "zonal", 10), (x8, u8, "zonal", 21), (x8, u8, "zonal", 32),
+                   (x8, u8, "uniform", 0), (x10, u10, "uniform", 0)]
+    refs = [oc.codec_images(a, m, r=max(r, 1), step=16, bit_depth=10 if a.dtype == np.int16 else 8)
+            for _, a, m, r in codec_cases]
+    streams = [torch.cuda.Stream(DEV) for _ in range(3 + len(codec_cases))]
+    for _ in range(3):
+        c8 = torch.empty((z8.shape[0], 16, 16), dtype=torch.int32, device=DEV)
+        c16 = torch.empty((z8.shape[0], 16, 16), dtype=torch.int16, device=DEV)
+        c10 = torch.empty((z10.shape[0], 16, 16), dtype=torch.int32, device=DEV)
+        outs = []
+        torch.cuda.synchronize()
+        with torch.cuda.stream(streams[0]):
+            pkg.dct16a_forward(x8, c8, pkg.desc_of(x8), streams[0])
+        with torch.cuda.stream(streams[1]):
+            pkg.dct16a_forward16(x8, c16, pkg.desc_of(x8), streams[1])
+        with torch.cuda.stream(streams[2]):
+            pkg.dct16a_forward(x10, c10, pkg.desc_of(x10, 10), streams[2])
+        for (x, a, m, r), s in zip(codec_cases, streams[3:]):
+            rec = torch.empty_like(x)
+            sse = torch.empty(x.shape[0], dtype=torch.int64, device=DEV)
+            with torch.cuda.stream(s):
+                pkg.dct16a_codec(x, pkg.make_quant(m, max(r, 1), 16), sse, rec, None,
+                                 pkg.desc_of(x, 10 if a.dtype == np.int16 else 8), s)
+            outs.append((rec, sse))
+        torch.cuda.synchronize()
+        assert np.array_equal(c8.cpu().numpy(), z8)
+        got16 = c16.cpu().numpy().astype(np.int64)
+        got16[:, 0, 0] &= 0xFFFF
+        assert np.array_equal(got16, z8)
+        assert np.array_equal(c10.cpu().numpy(), z10)
+        for (rec, sse), ref in zip(outs, refs):
+            assert np.array_equal(rec.cpu().numpy(), ref["recon_img"])
+            assert sse.cpu().tolist() == ref["sse"]
+
+
 def test_forward_concurrent_streams():
     """Eight dct16a_forward launches in flight on eight streams (the dynamic
     tile scheduler hands each launch its own counter slot) and 100 launches
