@@ -56,6 +56,9 @@
 namespace dct16a {
 namespace {
 
+#ifndef DCT16A_CW_PROMO
+#define DCT16A_CW_PROMO 3   // input L2 promotion (CUtensorMapL2promotion): 256 B
+#endif
 #ifndef DCT16A_CW_STAGES
 #define DCT16A_CW_STAGES 3
 #endif
@@ -462,7 +465,7 @@ int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon
     const uint32_t box[3] = {uint32_t(128 / ELEM), 16u, 1u};
     const CUtensorMapDataType dt = ELEM == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
     if (encode_tiled(&tin, dt, 3, src, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
+                     static_cast<CUtensorMapL2promotion>(DCT16A_CW_PROMO)))
         return DCT16A_ECUDA;
     if (recon) {
         if (encode_tiled(&tout, dt, 3, recon, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B,

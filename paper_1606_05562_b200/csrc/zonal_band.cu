@@ -84,6 +84,9 @@ __device__ __forceinline__ F2 operator-(F2 a, F2 b) { return F2{__fadd2_rn(a.v, 
 __device__ __forceinline__ F2 operator-(F2 a) { return F2{make_float2(-a.v.x, -a.v.y)}; }
 __device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) { return F2{__ffma2_rn(a.v, b.v, c.v)}; }
 
+#ifndef DCT16A_ZB_PROMO
+#define DCT16A_ZB_PROMO 0   // input L2 promotion: none (256 B promotion re-reads ~20 % of the input)
+#endif
 #ifndef DCT16A_ZB_CLAIM
 #define DCT16A_ZB_CLAIM 8
 #endif
@@ -331,7 +334,7 @@ int launch_zb(const void* src, const Geom& g, int r, void* recon, uint64_t* sse,
     const uint64_t strides[2] = {uint64_t(g.pitch), uint64_t(g.istride)};
     const uint32_t box[3] = {128u, 16u, 1u};
     if (encode_tiled(&tin, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, src, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
+                     static_cast<CUtensorMapL2promotion>(DCT16A_ZB_PROMO)))
         return DCT16A_ECUDA;
     if (recon) {
         if (encode_tiled(&tout, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, recon, dims, strides, box,
