@@ -142,6 +142,7 @@ DCT16A_API int dct16a_inverse(const int32_t* qcoef, const dct16a_desc* desc,
  *   ref, test : two image batches with the same *desc.
  *   sse       : uint64 out [batch] (exact).
  *   psnr      : optional float64 out [batch] (may be NULL).
+ * DCT16A_ESHAPE if one image's valid region is 32 GiB or more.
  */
 DCT16A_API int dct16a_psnr(const void* ref, const void* test, const dct16a_desc* desc,
                            uint64_t* sse, double* psnr, void* stream);

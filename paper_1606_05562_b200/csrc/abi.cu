@@ -228,6 +228,9 @@ DCT16A_API int dct16a_psnr(const void* ref, const void* test, const dct16a_desc*
     if (!sse) return fail(DCT16A_ENULL, "sse is NULL");
     if (reinterpret_cast<uintptr_t>(sse) & 7u) return fail(DCT16A_EALIGN, "sse is not 8-byte aligned");
     if (psnr && (reinterpret_cast<uintptr_t>(psnr) & 7u)) return fail(DCT16A_EALIGN, "psnr not 8-byte aligned");
+    if (static_cast<long long>(g.VH) * g.W * g.elem / 16 >= (1LL << 31))
+        return fail(DCT16A_ESHAPE, "valid_height*width*elem = %lld bytes per image: dct16a_psnr takes < 32 GiB",
+                    static_cast<long long>(g.VH) * g.W * g.elem);
     return launched(launch_psnr(ref, test, g, sse, psnr, static_cast<cudaStream_t>(stream)), "dct16a_psnr");
 }
 

@@ -348,36 +348,32 @@ __global__ void __launch_bounds__(kCodecWarps * 32) codec_kernel(const uint8_t* 
 // ------------------------------------------------------------------ K6
 __global__ void sse_kernel(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b,
                            unsigned long long* sse, const Geom g) {
-    const int cpr = g.W * g.elem / 16;   // 16-byte chunks per row
+    const uint32_t cpr = static_cast<uint32_t>(g.W * g.elem / 16);   // 16-byte chunks per row
     __shared__ uint64_t ws[32];
     for (int n = blockIdx.y; n < g.N; n += gridDim.y) {   // gridDim.y <= 65535: stride over images
-    const long long total = static_cast<long long>(g.VH) * cpr;
+    // chunks of one image: VH·cpr < 2^31 (validated by the launcher), so 32-bit index arithmetic
+    const uint32_t total = static_cast<uint32_t>(g.VH) * cpr;
     uint64_t acc = 0;
-    for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < total;
-         c += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long row = c / cpr;
-        const int col = static_cast<int>(c - row * cpr);
-        const long long off = n * g.istride + row * g.pitch + col * 16LL;
-        const uint4 va = *reinterpret_cast<const uint4*>(a + off);
-        const uint4 vb = *reinterpret_cast<const uint4*>(b + off);
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
+        const uint32_t row = c / cpr;
+        const uint32_t col = c - row * cpr;
+        const long long off = n * g.istride + static_cast<long long>(row) * g.pitch + col * 16LL;
+        const uint4 va = __ldcs(reinterpret_cast<const uint4*>(a + off));
+        const uint4 vb = __ldcs(reinterpret_cast<const uint4*>(b + off));
         const uint32_t wa[4] = {va.x, va.y, va.z, va.w}, wb[4] = {vb.x, vb.y, vb.z, vb.w};
+        uint32_t e = 0;   // <= 16·255² (8-bit) or 8·1023² (10-bit): fits 32 bits
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             if (g.elem == 1) {
-#pragma unroll
-                for (int s = 0; s < 4; ++s) {
-                    const int d = static_cast<int>((wa[q] >> (8 * s)) & 0xFF) - static_cast<int>((wb[q] >> (8 * s)) & 0xFF);
-                    acc += static_cast<uint32_t>(d * d);
-                }
+                const uint32_t d = __vabsdiffu4(wa[q], wb[q]);   // |x - y| per byte
+                e = __dp4a(d, d, e);
             } else {
-#pragma unroll
-                for (int s = 0; s < 2; ++s) {
-                    const int d = static_cast<int>(static_cast<int16_t>((wa[q] >> (16 * s)) & 0xFFFF)) -
-                                  static_cast<int>(static_cast<int16_t>((wb[q] >> (16 * s)) & 0xFFFF));
-                    acc += static_cast<uint64_t>(static_cast<int64_t>(d) * d);
-                }
+                const uint32_t d = __vabsdiffu2(wa[q], wb[q]);   // |x - y| per 16-bit pixel (both in [0, 1023])
+                const uint32_t lo = d & 0xFFFFu, hi = d >> 16;
+                e += lo * lo + hi * hi;
             }
         }
+        acc += e;
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
