@@ -182,3 +182,14 @@ def test_build_flags_keep_subnormals():
     assert "fast_math" not in flags and "ftz=true" not in flags
     src = open(os.path.join(ROOT, "paper_1606_05562_b200", "csrc", "ptx.cuh")).read()
     assert "mul.rm.f32x2" in src and "mul.rm.ftz" not in src
+
+
+def test_psnr_rejects_huge_valid_region():
+    """dct16a_psnr indexes 16-byte chunks of one image in 32 bits: a valid
+    region of 32 GiB or more is a shape error, raised before any launch."""
+    L = pkg.lib()
+    W, H = 1 << 20, 1 << 15
+    d = _lib.Desc(W, H, H, 1, 8, 0, W, W * H)
+    buf = ctypes.c_void_p(1 << 20)
+    assert L.dct16a_psnr(buf, buf, ctypes.byref(d), buf, None, None) == -2
+    assert "32 GiB" in pkg.dct16a_last_error()
