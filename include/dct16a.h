@@ -7,9 +7,12 @@
  * Every entry point is asynchronous on the given CUDA stream (`stream` is a
  * cudaStream_t passed as void*; NULL = legacy default stream).  All data
  * pointers are DEVICE pointers unless the name says `host`.  The caller owns
- * and frees every buffer; the library never allocates device memory, never
- * synchronises the stream and keeps no per-call state (constants live in
- * __constant__ memory).  Calls are thread-safe and re-entrant.
+ * and frees every buffer; the library never allocates device memory and
+ * never synchronises the stream.  Constants live in __constant__ memory; the
+ * only state is the dynamic tile schedulers' counters (static __device__
+ * arrays of 64 slots per kernel family, taken round-robin by successive calls
+ * and reset by each launch's last warp: see dct16a_forward and dct16a_codec).
+ * Calls are thread-safe and re-entrant.
  *
  * Errors: every function validates all arguments synchronously before any
  * launch and returns 0 on success or a negative DCT16A_E* code, leaving the
