@@ -259,6 +259,9 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
         __syncwarp();
 
         // ---- inverse along row i of both blocks, pixels, SSE, in-place reconstruction
+        // (the tile's SSE in 32 bits: at most 4 rows x 16 x 255^2 per lane)
+        uint32_t etile = 0;
+        const uint32_t m0 = valid0 ? 0xFFFFFFFFu : 0u, m1 = valid1 ? 0xFFFFFFFFu : 0u;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int i = r8 + 8 * h;
@@ -296,10 +299,11 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
                     const uint32_t dd = __vabsdiffu4(o[c4], ow[c4]);
                     e = __dp4a(dd, dd, e);
                 }
-                if ((blk ? valid1 : valid0) && row_ok) acc += e;
+                etile += e & (blk ? m1 : m0) & (row_ok ? 0xFFFFFFFFu : 0u);
                 if (p.has_recon) *cell = make_uint4(o[0], o[1], o[2], o[3]);
             }
         }
+        acc += etile;
         __syncwarp();
         if (lane == 0) {
             if (p.has_recon) {
