@@ -5,28 +5,29 @@
 // per-image SSE (906-910).
 //
 // A warp owns one 8-block tile (16 rows x 128 px, tile128.cuh) per iteration;
-// lane = (block b = lane & 7, quarter q = lane >> 3).  Only the anti-diagonal
-// band k + l <= BAND that holds the first r zig-zag positions is computed
-// (BAND 3/5/7 is a template parameter; the compiler removes every network
-// output outside the band and every zero input of the inverse).
-// * Row pass (SWAR): lane (b, q) runs rows (q, q+8) and (q+4, q+12) of block b
-//   as two 16-bit lanes of one 32-bit word (lo + hi·2^16 is linear under ±),
-//   so 128 rows take 2 networks per lane; outputs l <= BAND, biased by 2^15 so
-//   the halves are non-negative and are repacked by PRMT into column-pair words
-//   (Y[t][2p], Y[t][2p+1]) — the transposition buffer of PAPER.md:1082-1090 is
-//   a per-warp smem tile.
-// * Column pass (SWAR): lane (b, p = q) runs column pair (2p, 2p+1) down the 16
-//   rows, outputs k <= BAND; Z_00 in [0, 65280] is decoded unsigned, every other
-//   Z in int16 (the K1 ranges).  W = 2304/(g_k g_l) on the zonal cells, the
-//   rounding offset 1152 on the DC input: every pixel of the inverse is N + 1152.
-// * Inverse in float32, exact, on N·2^-35: every input W·Z (+1152) and every
-//   value the transposed network forms is an integer of magnitude < 1.59e6
-//   (< 2^21) for 8-bit input and r <= 36 — the exact maximum of each value, a
-//   linear function of the block, over [0, 255]^256 (tests/
-//   test_exactness_bounds.py) — times 2^-35: a normal float held exactly.  Lane (bp, l) runs the transposed
-//   network down column l of both blocks (FADD2; inputs k <= BAND, the others
-//   compile-time zeros), the smem tile turns columns into rows, lane (bp, r8)
-//   runs rows r8, r8+8 of both blocks (inputs l <= BAND).
+// lane = (block pair bp = lane >> 3: blocks bp and bp + 4 of the tile,
+// r8 = lane & 7).  Only the anti-diagonal band k + l <= BAND that holds the
+// first r zig-zag positions is computed (BAND 3/5/7 is a template parameter;
+// the compiler removes every network output outside the band and every zero
+// input of the inverse, net16.cuh net_inv_head).
+// * Row pass (SWAR): lane (bp, r8) runs row t = r8 and t = r8 + 8 of blocks bp
+//   and bp + 4 as the two 16-bit lanes of one 32-bit word per pixel (lo + hi·2^16
+//   is linear under ±, mod 2^32), outputs l <= BAND; the raw SWAR words go to a
+//   per-warp smem tile (the transposition buffer of PAPER.md:1082-1090).
+// * Column pass (SWAR): lane (bp, l = r8) runs column l of both blocks down the
+//   16 rows on the same words, outputs k <= BAND; only Z is decoded: Z_00 in
+//   [0, 65280] zero-extended, every other Z sign-extended from int16 (the K1
+//   ranges).  W = 2304/(g_k g_l) on the zonal cells, the rounding offset 1152 on
+//   the DC input: every pixel of the inverse is N + 1152.
+// * Inverse in float32 pairs (FADD2/FFMA2: block bp in .x, block bp + 4 in .y),
+//   exact, on N·2^-35: every input W·Z (+1152) and every value the transposed
+//   network forms is an integer of magnitude < 1.59e6 (< 2^21) for 8-bit input
+//   and r <= 36 — the exact maximum of each value, a linear function of the
+//   block, over [0, 255]^256 (tests/test_exactness_bounds.py) — times 2^-35: a
+//   normal float held exactly.  Lane (bp, l) runs the transposed network down
+//   column l (inputs k <= BAND, the others compile-time zeros), the smem tile
+//   turns columns into rows, lane (bp, r8) runs rows r8, r8 + 8 (inputs
+//   l <= BAND).
 // * Pixel = floor((N + 1152)/2304) by ONE round-down multiply per two pixels
 //   (FMUL2.RM) with c = fl(2^-114/2304): the exact product (N/2304)·2^-149·(1+δ)
 //   rounded down to the subnormal grid is floor(N·fl(1/2304))·2^-149, whose bit
