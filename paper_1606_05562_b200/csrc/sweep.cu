@@ -37,6 +37,10 @@
 namespace dct16a {
 namespace {
 
+#ifndef DCT16A_SWEEP_UNROLL
+#define DCT16A_SWEEP_UNROLL 8
+#endif
+constexpr int kSweepUnroll = DCT16A_SWEEP_UNROLL;   // measured r-loop unroll
 constexpr int kSWarps = 4;    // warps per CTA
 constexpr int kSStages = 3;   // TMA ring depth per warp
 
@@ -226,7 +230,7 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) tq[q] = tqn[q];
             }
-#pragma unroll 1
+#pragma unroll kSweepUnroll
             for (int r = p.r_first; r <= p.r_last; ++r) {
                 float svn;
                 float4 tqn[4];
