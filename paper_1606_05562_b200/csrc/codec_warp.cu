@@ -377,13 +377,18 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
                         pix[j] = __vimin_s32_relu(__double2hiint(d) - 0x41380000, p.maxpix);
                     }
                     if (!valid) nmin = 0xFFFFFFFFu;
-                    if (__any_sync(0xffffffffu, nmin < 8192u) && nmin < 8192u) {
-                        int fix[16];   // local memory, rare branch only
+                    if (__any_sync(0xffffffffu, nmin < 8192u)) {
+                        if (nmin < 8192u) {
+                            int fix[16];   // local memory, rare branch only
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) fix[j] = pix[j];
-                        exact_row_fix<ELEM>(stage, bb, tu + t * 17, t, p.step, p.maxpix, fix);
+                            for (int j = 0; j < 16; ++j) fix[j] = pix[j];
+                            exact_row_fix<ELEM>(stage, bb, tu + t * 17, t, p.step, p.maxpix, fix);
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) pix[j] = fix[j];
+                            for (int j = 0; j < 16; ++j) pix[j] = fix[j];
+                        }
+                        // the exact fix re-reads the whole block's ORIGINAL pixels from the
+                        // stage: no lane may overwrite its row with the reconstruction before
+                        __syncwarp();
                     }
                 } else {
                     // floor((N + 1152.5)/2304) by one round-down FMA onto 2^23 (exact: the
