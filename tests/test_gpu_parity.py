@@ -395,6 +395,21 @@ def test_config3_full_size_sampled():
         assert abs(float(ps[f]) - ref["psnr"][0]) < 1e-3
 
 
+@pytest.mark.parametrize("frames", [24])
+def test_codec_mid_size_claim_runs(frames):
+    """Mid-size launches, where the tile claims are shorter than the default
+    run (2-5 tiles for the band kernel, 3-4 for the warp kernel): every frame's
+    SSE and every reconstruction against the oracle, zonal and uniform."""
+    v = synth.video_u8(frames)
+    x = to_dev(v)
+    for mode in ("zonal", "uniform"):
+        rec, sse, _ = pkg.codec(x, mode, r=32, step=16, valid_height=1080)
+        torch.cuda.synchronize()
+        ref = oc.codec_images(v, mode, r=32, step=16, valid_height=1080)
+        assert np.array_equal(rec.cpu().numpy(), ref["recon_img"]), mode
+        assert sse.cpu().tolist() == ref["sse"], mode
+
+
 # ------------------------------------------------------ config 5: r-sweep
 def _sweep_check(imgs, bd, r_first, r_count, valid_height=None):
     x = to_dev(imgs)
