@@ -476,3 +476,107 @@ def test_ssim_against_straight_line_loops():
     f = synth.frame_10bit(3, H=16, W=16)
     g = np.clip(f.astype(int) + 7, 0, 1023)
     assert oq.ssim(f[None], g[None], bit_depth=10)[0] == pytest.approx(oq.ssim_bruteforce(f, g, 10), abs=1e-12)
+
+
+# ------------------------------------------------- whole-image block tiling
+# Pins of oracle.codec.to_blocks / from_blocks themselves (PAPER.md:866-869:
+# the image is split into disjoint 16x16 blocks A_k; reading A3: all blocks,
+# row-major; reading A5: Z = T·X·Tᵀ with X's first index the image row).
+# These go through whole images, so an in-block transpose or a swapped block
+# order inside the tiler fails them.
+
+def test_to_blocks_matches_pixel_loops():
+    rng = np.random.default_rng(21)
+    imgs = rng.integers(0, 256, size=(2, 48, 80))          # 3 x 5 blocks, non-square
+    Xb = oc.to_blocks(imgs)
+    assert Xb.shape == (2, 3, 5, 16, 16)
+    for n in range(2):
+        for by in range(3):
+            for bx in range(5):
+                for i in range(16):
+                    for j in range(16):
+                        assert Xb[n, by, bx, i, j] == imgs[n, 16 * by + i, 16 * bx + j]
+    assert np.array_equal(oc.from_blocks(Xb), imgs)
+    # from_blocks on its own: block (by, bx) entry (i, j) lands at pixel (16by+i, 16bx+j)
+    blk = np.arange(2 * 3 * 5 * 256).reshape(2, 3, 5, 16, 16)
+    img = oc.from_blocks(blk)
+    for n, by, bx, i, j in [(0, 0, 0, 0, 1), (1, 2, 4, 15, 0), (0, 1, 3, 2, 9), (1, 0, 2, 7, 15)]:
+        assert img[n, 16 * by + i, 16 * bx + j] == blk[n, by, bx, i, j]
+
+
+def test_whole_image_horizontal_ramp_has_energy_in_row_zero_only():
+    # X[i][j] = j + c_b inside block b: X = 1·(j + c_b)ᵀ, so Z = (T·1)(T·(j+c_b))ᵀ.
+    # T·1 = 16·e₀ (row 0 of T is all ones; every other row is
+    # orthogonal to it), hence only the row k = 0 (vertical frequency 0) of Z
+    # is non-zero, and Z[0][0] = 16·(120 + 16·c_b) with c_b = by·BX + bx.
+    BY, BX = 3, 4
+    img = np.zeros((1, 16 * BY, 16 * BX), dtype=np.int64)
+    for by in range(BY):
+        for bx in range(BX):
+            img[0, 16 * by:16 * by + 16, 16 * bx:16 * bx + 16] = np.arange(16)[None, :] + (by * BX + bx)
+    Z = oc.forward(oc.to_blocks(img))
+    assert np.count_nonzero(Z[..., 1:, :]) == 0
+    assert np.count_nonzero(Z[..., 0, 1:]) > 0
+    c = np.arange(BY * BX).reshape(BY, BX)
+    assert np.array_equal(Z[0, :, :, 0, 0], 16 * (120 + 16 * c))
+    # the vertical ramp puts its energy in column l = 0 only
+    Zv = oc.forward(oc.to_blocks(img.transpose(0, 2, 1).copy()))
+    assert np.count_nonzero(Zv[..., :, 1:]) == 0
+
+
+def test_whole_image_in_block_mirrors():
+    # Mirroring every block left-right inside the image gives Z·(-1)^l and
+    # top-bottom gives Z·(-1)^k: T[l][15-j] = (-1)^l·T[l][j] (even/odd rows of
+    # T) with l the horizontal frequency (reading A5).
+    imgs = synth.image_u8(5, 64, 96)[None].astype(np.int64)
+    mir_h = imgs.reshape(1, 4, 16, 6, 16)[:, :, :, :, ::-1].reshape(imgs.shape)
+    mir_v = imgs.reshape(1, 4, 16, 6, 16)[:, :, ::-1, :, :].reshape(imgs.shape)
+    Z = oc.forward(oc.to_blocks(imgs))
+    sgn = (-1) ** np.arange(16)
+    assert np.array_equal(oc.forward(oc.to_blocks(mir_h)), Z * sgn[None, None, None, None, :])
+    assert np.array_equal(oc.forward(oc.to_blocks(mir_v)), Z * sgn[None, None, None, :, None])
+    # and the two are distinguishable on this input (odd k and odd l both present)
+    assert np.any(Z[..., 1::2, :] != 0) and np.any(Z[..., :, 1::2] != 0)
+    assert not np.array_equal(Z * sgn[None, None, None, None, :], Z * sgn[None, None, None, :, None])
+
+
+def test_codec_images_keeps_horizontal_detail_in_first_row():
+    # The zonal pipeline through the tiler: a per-block horizontal ramp keeps
+    # only (0, l) coefficients, and zig-zag r = 3 keeps (0,0),(0,1),(1,0)
+    # (reading A4), so the reconstruction depends on j only inside each block.
+    img = np.tile(np.arange(16, dtype=np.int64) * 8 + 40, (1, 32, 2))
+    rec = oc.codec_images(img, "zonal", r=3)["recon_img"]
+    assert np.all(rec == rec[:, :1, :])                        # constant down each column
+    assert rec[0, 0, 0] < rec[0, 0, 15]                        # the ramp survives along j
+
+
+# -------------------------------------------------------- SSIM window sigma
+def test_ssim_window_is_gaussian_sigma_1p5():
+    # Wang et al. 2004 (the source PAPER.md:911-917 cites; reading A21): an
+    # 11x11 circular-symmetric Gaussian with standard deviation 1.5 samples,
+    # normalised to unit sum.  Check the taps against the library Gaussian
+    # filter (scipy.ndimage, sigma = 1.5, radius 5) applied to an impulse.
+    from scipy import ndimage
+    imp = np.zeros((11, 11))
+    imp[5, 5] = 1.0
+    ref = ndimage.gaussian_filter(imp, sigma=1.5, truncate=5 / 1.5, mode="constant")
+    assert np.max(np.abs(oq.gaussian_window() - ref)) < 1e-15
+    w = oq.gaussian_window()
+    # neighbour / centre tap = exp(-1/(2·1.5²)) = exp(-1/4.5) = 0.80073740...
+    assert w[5, 6] / w[5, 5] == pytest.approx(0.8007374029168081, rel=1e-14)
+    assert w[0, 0] / w[5, 5] == pytest.approx(math.exp(-50 / 4.5), rel=1e-12)
+
+
+def test_ssim_against_library_gaussian_filter():
+    # An independent SSIM: local moments from scipy.ndimage.gaussian_filter
+    # (sigma 1.5, 11 taps), cropped to the fully contained windows.
+    from scipy import ndimage
+    rng = np.random.default_rng(31)
+    x = synth.image_u8(6, 40, 56).astype(np.float64)
+    y = np.clip(x + rng.integers(-25, 26, size=x.shape), 0, 255)
+    f = lambda a: ndimage.gaussian_filter(a, sigma=1.5, truncate=5 / 1.5, mode="constant")[5:-5, 5:-5]
+    C1, C2 = (0.01 * 255) ** 2, (0.03 * 255) ** 2
+    mx, my = f(x), f(y)
+    vx, vy, cxy = f(x * x) - mx * mx, f(y * y) - my * my, f(x * y) - mx * my
+    m = ((2 * mx * my + C1) * (2 * cxy + C2)) / ((mx * mx + my * my + C1) * (vx + vy + C2))
+    assert oq.ssim(x.astype(np.uint8)[None], y.astype(np.uint8)[None])[0] == pytest.approx(m.mean(), abs=1e-12)
