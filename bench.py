@@ -1,24 +1,37 @@
 #!/usr/bin/env python
 """bench.py — throughput of the batched 16x16 approximate-DCT hot path.
 
-Workload (BASELINE.json configs[1], "config 2"): 4096 AR(1) (rho = 0.95)
+Headline (BASELINE.json configs[1], "config 2"): 4096 AR(1) (rho = 0.95)
 512x512 uint8 images (synth seeds 0..4095, 4,194,304 blocks); one step = the
 forward 2-D integer transform Z = T·X·Tᵀ of every block with int32 output
-(dct16a_forward, one kernel launch).  Inputs (1 GiB) and outputs (4 GiB) are
-far larger than the 126 MB L2, so no flush is needed between steps.
+(dct16a_forward, one kernel launch per rank).  Inputs (1 GiB) and outputs
+(4 GiB) are far larger than the 126 MB L2, so no flush is needed.
 
-Multi-GPU (torchrun): weak scaling — every rank runs the full config-2 batch on
-its own GPU; there is no data-path collective (frames/images are independent);
-value = blocks of all ranks / max over ranks of the device time.
+Multi-GPU (torchrun): the 4096 images are sharded
+contiguously, 4096/N per rank (strong scaling: the total work is fixed); there
+is no data-path collective; value = 4,194,304 blocks / max over ranks of the
+device time.
+
+The same line carries the fused paths of the other configs, each timed the
+same way (CUDA events on the launching stream, max over ranks):
+  cfg3 — 600 frames 1920x1088 u8 video, fused zonal r = 32, per-frame PSNR
+         (rank 0 generates the video, NCCL broadcast, 600/N frames per rank);
+  cfg4 — 1000 frames 3840x2160 10-bit, fused uniform Δ = 16 with the recon
+         written, then the path's one collective: the NCCL SUM all-reduce of
+         the per-frame SSE vector, and the library's PSNR finaliser; 1000/N
+         frames per rank (frame f holds fixture f mod 64: 64 distinct AR(1)
+         frames of the A14 recipe keep fixture generation within the bench
+         budget; 1 GB of distinct frames, far above L2);
+  cfg5 — r-sweep r = 1..256 over 64 images 1024x1024 (64/N per rank).
+At N = 1 each entry also carries the CPU oracle's rate on a bounded sample.
 
 --impl reference: the CPU oracle (oracle/codec.py, numpy float64) timed on the
-host cores on a bounded sample of the same workload, rank 0 only.
+host cores on a bounded sample of the config-2 workload, rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import sys
@@ -31,10 +44,13 @@ sys.path.insert(0, ROOT)
 METRIC = "16x16 2-D approx-DCT blocks/s and HBM GB/s (fraction of B200 peak), 1/2/4/8 GPUs"
 # best no-compute kernel for K1's 20/80 read/write byte mix on this box type (measured, round 1)
 MIX_CEILING_GBS = 6799.0
+# issue peak for instruction-bound kernels: 4 warp-instructions/clock/SM x 148 SMs x 1.965 GHz
+ISSUE_PEAK = 4 * 148 * 1.965e9
 N_IMG, H, W = 4096, 512, 512
 BLOCKS_PER_IMG = (H // 16) * (W // 16)
 BYTES_PER_BLOCK = 256 + 1024          # u8 block in + int32 block out
 WORKLOAD = "config 2: 4096 x 512x512 uint8 AR(1) rho=0.95 images, forward 2-D integer transform, int32 out"
+CFG4_DISTINCT = 64
 
 
 def peaks():
@@ -43,6 +59,17 @@ def peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:  # pragma: no cover
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 class ClockSampler:
@@ -98,80 +125,260 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
-# ------------------------------------------------------------ CPU oracle leg
-_IMGS = None   # config-2 sample, inherited by forked oracle workers
+# ------------------------------------------------------------ CPU oracle legs
+_ITEMS = None   # the sample, inherited by forked oracle workers
 
 
-def _oracle_worker_init():
+def _oracle_init():
     from threadpoolctl import threadpool_limits
     global _LIMIT
     _LIMIT = threadpool_limits(1)
 
 
-def _oracle_forward_chunk(rng):
+def _oracle_job(args):
+    """One item of the sample through the oracle as it stands; returns units
+    (blocks, or block-evaluations for the r-sweep)."""
     import numpy as np
     from oracle import codec as oc
-    a, b = rng
-    oc.forward(oc.to_blocks(_IMGS[a:b].astype(np.int64)))
-    return (b - a) * BLOCKS_PER_IMG
+    kind, i = args
+    img = _ITEMS[i:i + 1]
+    n, h, w = img.shape
+    blocks = n * (h // 16) * (w // 16)
+    if kind == "cfg2":
+        oc.forward(oc.to_blocks(img.astype(np.int64)))
+    elif kind == "cfg3":
+        oc.codec_images(img, "zonal", r=32, valid_height=1080)
+    elif kind == "cfg4":
+        oc.codec_images(img, "uniform", step=16, bit_depth=10)
+    elif kind == "cfg5":
+        for r in range(1, 257):
+            oc.codec_images(img, "zonal", r=r)
+        blocks *= 256
+    return blocks
 
 
-def oracle_rate(n_images: int, workers: int):
-    """Oracle forward (oracle.codec.forward, dense float64 T·X·Tᵀ, as it
-    stands) over the first n_images config-2 images, split across `workers`
-    forked processes with one BLAS thread each.  Returns (blocks/s over wall
-    time, CPU seconds, wall seconds)."""
+def oracle_rate(kind: str, items, workers: int):
+    """The oracle over `items` (one job per image/frame) on `workers` forked
+    processes with one BLAS thread each: (units/s over wall, CPU-s, wall-s)."""
     import multiprocessing as mp
-
-    import synth
-    global _IMGS
-    if _IMGS is None or len(_IMGS) < n_images:
-        _IMGS = synth.batch_u8(range(n_images), H, W)
-    chunks = [(i, min(n_images, i + 4)) for i in range(0, n_images, 4)]
+    global _ITEMS
+    _ITEMS = items
     ctx = mp.get_context("fork")
-    with ctx.Pool(workers, initializer=_oracle_worker_init) as pool:
-        pool.map(_oracle_forward_chunk, [(0, 1)] * workers)            # warm the workers
-        c0, t0 = time.process_time(), time.perf_counter()
-        blocks = sum(pool.map(_oracle_forward_chunk, chunks, chunksize=1))
+    jobs = [(kind, i) for i in range(len(items))]
+    with ctx.Pool(min(workers, len(jobs)), initializer=_oracle_init) as pool:
+        pool.map(_oracle_job, [("cfg2", 0)] * min(workers, len(jobs)))     # warm the workers
+        t0 = time.perf_counter()
+        units = sum(pool.map(_oracle_job, jobs, chunksize=1))
         wall = time.perf_counter() - t0
-    return blocks / wall, wall * workers, wall
+    return units / wall, wall * min(workers, len(jobs)), wall
 
 
 def run_reference(args):
+    import synth
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     workers = host_cores()
     steps, warm = args.steps, args.warmup
     # size each step so the whole run stays within about a minute of wall time
-    per_step_images = max(workers, min(512, int(60.0 * workers * 70.0 / (steps + warm))))
+    per_step = max(workers, min(512, int(60.0 * workers * 70.0 / (steps + warm))))
+    imgs = synth.batch_u8(range(per_step), H, W)
     rates = []
     for i in range(warm + steps):
-        r, _, _ = oracle_rate(per_step_images, workers)
+        r, _, _ = oracle_rate("cfg2", imgs, workers)
         if i >= warm:
             rates.append(r)
     value = statistics.median(rates)
-    ms = per_step_images * BLOCKS_PER_IMG / value * 1e3
+    ms = per_step * BLOCKS_PER_IMG / value * 1e3
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "blocks/s",
             "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "global_batch": per_step_images,
-                                            "sample": f"{per_step_images} images per step"},
-            "cpu_baseline": {"value": value, "unit": "blocks/s", "cores": workers, "kind": "oracle",
-                             "sample": f"{per_step_images} of the 4096 config-2 images per step, "
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "global_batch": per_step,
+                                            "sample": f"{per_step} images per step"},
+            "cpu_baseline": {"value": value, "unit": "blocks/s", "cores": workers, "cpu": cpu_model(),
+                             "kind": "oracle",
+                             "sample": f"{per_step} of the 4096 config-2 images per step, "
                                        "oracle.codec.forward (dense float64 T·X·Tᵀ), one process per core"},
             "e2e": {"value": value, "unit": "blocks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-# ----------------------------------------------------------------- GPU leg
+# ----------------------------------------------------------------- GPU legs
+class Ctx:
+    def __init__(self, torch, dist, world, rank, dev):
+        self.torch, self.dist, self.world, self.rank, self.dev = torch, dist, world, rank, dev
+        self.stream = torch.cuda.current_stream(dev)
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max_over_ranks(self, v: float) -> float:
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(self, step, steps: int, warmup: int, clocks=None):
+        """ms per step: CUDA events on the launching stream around `steps`
+        calls, barrier + synchronize on both sides, max over ranks."""
+        torch = self.torch
+        for _ in range(warmup):
+            step()
+        torch.cuda.synchronize()
+        self.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if clocks is not None:
+            clocks.__enter__()
+        e0.record(self.stream)
+        for _ in range(steps):
+            step()
+        e1.record(self.stream)
+        e1.synchronize()
+        if clocks is not None:
+            clocks.__exit__()
+        torch.cuda.synchronize()
+        self.barrier()
+        mine = e0.elapsed_time(e1)
+        return self.max_over_ranks(mine) / steps, mine / steps
+
+
+def leg_cfg3(c: Ctx, args, peak):
+    import paper_1606_05562_b200 as pkg
+    import synth
+    from paper_1606_05562_b200 import parallel
+    torch = c.torch
+    n_total = 600
+    if c.rank == 0:
+        video = torch.from_numpy(synth.video_u8(n_total)).to(c.dev)
+    else:
+        video = torch.empty((n_total, 1088, 1920), dtype=torch.uint8, device=c.dev)
+    if c.world > 1:
+        c.dist.broadcast(video, 0)
+    a, b = parallel.shard(n_total, c.world, c.rank)
+    x = video[a:b].contiguous()
+    del video
+    recon = torch.empty_like(x)
+    n = b - a
+    sse = torch.empty(n, dtype=torch.int64, device=c.dev)
+    psnr = torch.empty(n, dtype=torch.float64, device=c.dev)
+    d = pkg.desc_of(x, valid_height=1080)
+    q = pkg.make_quant("zonal", 32)
+    ms, _ = c.timed(lambda: pkg.dct16a_codec(x, q, sse, recon, psnr, d, c.stream), args.cfg_steps, 3)
+    blocks = n_total * 68 * 120
+    alg = blocks * 512
+    out = {"workload": "600 x 1920x1088 u8 AR(1) video, fused zonal r=32 + recon + per-frame PSNR (valid 1080 rows)",
+           "kernel": "zband_kernel<7>", "ms": ms, "blocks_per_s": blocks / ms * 1e3, "alg_bytes_per_block": 512,
+           "alg_GBs": alg / ms / 1e6, "bound": "hbm", "frac": alg / ms / 1e6 / peak,
+           "mean_psnr_db_rank0": float(psnr.mean().item())}
+    return out, (x[:24].cpu().numpy() if c.rank == 0 and c.world == 1 else None)
+
+
+def leg_cfg4(c: Ctx, args, peak):
+    import paper_1606_05562_b200 as pkg
+    import synth
+    from paper_1606_05562_b200 import parallel
+    torch = c.torch
+    n_total, K = 1000, CFG4_DISTINCT
+    # the K distinct fixture frames: rank r generates ids r, r + N, ... and one all_gather shares them
+    ids = list(range(c.rank, K, c.world))
+    per = (K + c.world - 1) // c.world
+    part = torch.zeros((per, 2160, 3840), dtype=torch.int16, device=c.dev)
+    if ids:
+        part[:len(ids)] = torch.from_numpy(synth.frames_10bit(ids, workers=max(1, host_cores() // c.world))).to(c.dev)
+    if c.world > 1:
+        parts = [torch.empty_like(part) for _ in range(c.world)]
+        c.dist.all_gather(parts, part)
+    else:
+        parts = [part]
+    distinct = torch.empty((K, 2160, 3840), dtype=torch.int16, device=c.dev)
+    for r in range(c.world):
+        cnt = len(range(r, K, c.world))
+        distinct[r::c.world] = parts[r][:cnt]
+    del parts, part
+    a, b = parallel.shard(n_total, c.world, c.rank)
+    n = b - a
+    x = distinct[torch.arange(a, b, device=c.dev) % K]            # frame f holds fixture f mod K
+    recon = torch.empty_like(x)
+    full = torch.zeros(n_total, dtype=torch.int64, device=c.dev)
+    psnr = torch.empty(n_total, dtype=torch.float64, device=c.dev)
+    tot = torch.empty(1, dtype=torch.int64, device=c.dev)
+    ptot = torch.empty(1, dtype=torch.float64, device=c.dev)
+    d = pkg.desc_of(x)
+    dframe = pkg.make_desc(3840, 2160, 1, 10)
+    q = pkg.make_quant("uniform", step=16)
+
+    def step():
+        full.zero_()
+        pkg.dct16a_codec(x, q, full[a:b], recon, None, d, c.stream)      # this rank's slice of the vector
+        if c.world > 1:
+            c.dist.all_reduce(full, op=c.dist.ReduceOp.SUM)               # the path's one exchange (NCCL)
+        pkg.dct16a_sse_psnr(full, n_total, dframe, psnr, tot, ptot, c.stream)
+
+    ms, _ = c.timed(step, args.cfg_steps, 3)
+    # the collective and finaliser alone (their share of the step)
+    def coll():
+        if c.world > 1:
+            c.dist.all_reduce(full, op=c.dist.ReduceOp.SUM)
+        pkg.dct16a_sse_psnr(full, n_total, dframe, psnr, tot, ptot, c.stream)
+    ms_coll, _ = c.timed(coll, 10, 3)
+    step()
+    torch.cuda.synchronize()
+    # invariance check: every frame's SSE is that of its fixture, so the
+    # all-reduced vector and ΣSSE are the same at every N
+    dsse = torch.empty(K, dtype=torch.int64, device=c.dev)
+    pkg.dct16a_codec(distinct, q, dsse, None, None, pkg.desc_of(distinct), c.stream)
+    want = dsse[torch.arange(n_total, device=c.dev) % K]
+    torch.cuda.synchronize()
+    ok = bool(torch.equal(full, want)) and int(tot.item()) == int(want.sum().item())
+    blocks = n_total * 135 * 240
+    alg = blocks * 1024
+    out = {"workload": "1000 x 3840x2160 10-bit frames (fixture f mod 64), fused uniform step 16 + recon, "
+                       "SSE all-reduce (NCCL SUM, 8 KB) + global PSNR finaliser",
+           "kernel": "codec_warp_kernel<2,1>", "ms": ms, "collective_and_finaliser_ms": ms_coll,
+           "blocks_per_s": blocks / ms * 1e3, "alg_bytes_per_block": 1024, "alg_GBs": alg / ms / 1e6,
+           "bound": "hbm", "frac": alg / ms / 1e6 / peak, "global_psnr_db": float(ptot.item()),
+           "sse_total": int(tot.item()), "sse_matches_fixtures": ok,
+           "collective": "nccl all_reduce" if c.world > 1 else "none (1 rank)"}
+    sample = distinct[:6].cpu().numpy() if c.rank == 0 and c.world == 1 else None
+    return out, sample
+
+
+def leg_cfg5(c: Ctx, args, peak):
+    import paper_1606_05562_b200 as pkg
+    import synth
+    from paper_1606_05562_b200 import parallel
+    torch = c.torch
+    a, b = parallel.shard(64, c.world, c.rank)
+    seeds = range(100 + a, 100 + b)
+    x = torch.from_numpy(synth.batch_u8(seeds, 1024, 1024, rho=synth.cfg5_rho,
+                                        workers=max(1, host_cores() // c.world))).to(c.dev)
+    n = b - a
+    sse = torch.empty((n, 256), dtype=torch.int64, device=c.dev)
+    psnr = torch.empty((n, 256), dtype=torch.float64, device=c.dev)
+    d = pkg.desc_of(x)
+    ms, _ = c.timed(lambda: pkg.dct16a_zonal_sweep(x, 1, 256, sse, psnr, d, c.stream), args.cfg_steps, 3)
+    blocks = 64 * 64 * 64
+    evals = blocks * 256
+    out = {"workload": "64 x 1024x1024 u8 (rho .85/.90/.95/.98), zonal r-sweep r=1..256, SSE/PSNR per r",
+           "kernel": "sweep_kernel<1>", "ms": ms, "blocks_per_s": blocks / ms * 1e3,
+           "block_evals_per_s": evals / ms * 1e3, "alg_GBs": blocks * 256 / ms / 1e6, "bound": "alu (issue)",
+           "note": "64 MiB of input, L2-resident; bounded by instruction issue, not HBM"}
+    sample = None
+    if c.rank == 0 and c.world == 1:   # 16 crops of 256x256 (one per rho group quarter) keep the oracle's sweep short
+        crops = x[:4, :512, :512].cpu().numpy().reshape(4, 2, 256, 2, 256).transpose(0, 1, 3, 2, 4)
+        sample = crops.reshape(16, 256, 256).copy()
+    return out, sample
+
+
 def run_ours(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_1606_05562_b200 as pkg
     import synth
+    from paper_1606_05562_b200 import parallel
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -180,118 +387,97 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-
-    # ---- inputs: config 2 (the same 4096 images on every rank: weak scaling).
-    # Generation is split across ranks (rank r draws seeds r, r+world, ...) and
-    # all-gathered once before timing, so N ranks do not each regenerate 1 GiB.
-    if world > 1:
-        from paper_1606_05562_b200 import parallel
-        mine = parallel.strided_ids(N_IMG, world, rank)
-        part = torch.from_numpy(synth.batch_u8(mine, H, W, workers=max(1, host_cores() // world))).to(dev)
-        x = parallel.allgather_strided(part, N_IMG, world)
-        del part
-        host = x.cpu().pin_memory()
-    else:
-        host = torch.from_numpy(synth.batch_u8(range(N_IMG), H, W)).pin_memory()
-        x = host.to(dev)
-    nblocks = N_IMG * BLOCKS_PER_IMG
-    coef = torch.empty((nblocks, 16, 16), dtype=torch.int32, device=dev)
-    desc = pkg.desc_of(x)
-    stream = torch.cuda.current_stream(dev)
-
-    def step():
-        pkg.dct16a_forward(x, coef, desc, stream)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        e1.synchronize()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms_total = e0.elapsed_time(e1)
-    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    ms_step = ms_max / args.steps
-    value = world * nblocks / (ms_step / 1e3)
-
-    # roofline of the dominant (only) kernel, measured on its launch stream
+    c = Ctx(torch, dist, world, rank, dev)
     peak, peak_src = peaks()
-    alg_bytes = nblocks * BYTES_PER_BLOCK
-    achieved = alg_bytes / (ms_total / args.steps / 1e3) / 1e9
+
+    # ---- headline: config 2, images [a, b) of 4096 on this rank (generated here)
+    a, b = parallel.shard(N_IMG, world, rank)
+    host = torch.from_numpy(synth.batch_u8(range(a, b), H, W, workers=max(1, host_cores() // world))).pin_memory()
+    x = host.to(dev)
+    nb_local = (b - a) * BLOCKS_PER_IMG
+    nblocks = N_IMG * BLOCKS_PER_IMG
+    coef = torch.empty((nb_local, 16, 16), dtype=torch.int32, device=dev)
+    desc = pkg.desc_of(x)
+
+    clk = ClockSampler(local)
+    ms_step, ms_mine = c.timed(lambda: pkg.dct16a_forward(x, coef, desc, c.stream), args.steps, args.warmup, clk)
+    value = nblocks / (ms_step / 1e3)
+
+    # roofline of the dominant (only) kernel, from this rank's own launch time on its stream
+    alg_bytes = nb_local * BYTES_PER_BLOCK
+    achieved = alg_bytes / (ms_mine / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and world == 1:
         traffic = json.load(open(tp)).get("fwd_kernel_u8_cfg2_bytes_per_launch")
 
-    # ---- end to end through the public API with pinned host buffers
-    host_coef = torch.empty((nblocks, 16, 16), dtype=torch.int32, pin_memory=True)
-    bufs = pkg.forward_host(host, host_coef, chunk_images=256)
+    # ---- end to end through the C entry dct16a_forward_host (pinned host buffers)
+    host_coef = torch.empty((nb_local, 16, 16), dtype=torch.int32, pin_memory=True)
+    ws = pkg.forward_host(host, host_coef, chunk_images=max(1, min(256, b - a)))
     torch.cuda.synchronize()
     e2e_steps = max(1, min(args.steps, 5))
-    if world > 1:
-        dist.barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    for _ in range(e2e_steps):
-        bufs = pkg.forward_host(host, host_coef, chunk_images=256, bufs=bufs)
-    f1.record(stream)
-    f1.synchronize()
-    te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * nblocks / (float(te.item()) / e2e_steps / 1e3)
-    # spot-check the host result against the device result (cheap)
+    ms_e2e, _ = c.timed(lambda: pkg.forward_host(host, host_coef, chunk_images=256, workspace=ws), e2e_steps, 0)
+    e2e_value = nblocks / (ms_e2e / 1e3)
     ok = torch.equal(host_coef[:1024].to(dev), coef[:1024])
+    del host_coef, host
 
-    line = None
+    # ---- the fused paths of configs 3, 4, 5
+    configs, samples = {}, {}
+    if not args.headline_only:
+        del coef, x
+        torch.cuda.empty_cache()
+        for name, fn in (("cfg3", leg_cfg3), ("cfg4", leg_cfg4), ("cfg5", leg_cfg5)):
+            configs[name], samples[name] = fn(c, args, peak)
+            torch.cuda.empty_cache()
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "blocks/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
                 "data": "synthetic",
-                "config": {"workload": WORKLOAD, "global_batch": world * N_IMG, "blocks_per_gpu": nblocks,
-                           "parallelism": f"dp{world} (independent images, no collective)",
+                "config": {"workload": WORKLOAD, "global_batch": N_IMG, "blocks": nblocks,
+                           "images_per_gpu": b - a,
+                           "parallelism": f"dp{world}: images sharded contiguously, 4096/{world} per GPU, "
+                                          "no collective (independent images)",
                            "l2": "inputs (1 GiB) and outputs (4 GiB) larger than L2; no flush"},
-                "hbm_gbs": achieved,
+                "hbm_gbs": nblocks * BYTES_PER_BLOCK / (ms_step / 1e3) / 1e9,
                 "roofline": {"kernel": "fwd_kernel<1,5>", "bound": "hbm", "achieved": achieved, "peak": peak,
                              "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                              "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
-                             "note": "peak = copy burst (50/50 read/write); this kernel moves 20/80 "
-                                     "read/write, for which the best no-compute kernel measured "
-                                     f"{MIX_CEILING_GBS:.0f} GB/s (tools/mix_ceiling.cu, "
-                                     "profiles/r01_fwd_dynamic_sched.md)",
+                             "note": "per launch on rank 0; peak = copy burst (50/50 read/write); this kernel "
+                                     "moves 20/80 read/write, for which the best no-compute kernel measured "
+                                     f"{MIX_CEILING_GBS:.0f} GB/s (tools/mix_ceiling.cu)",
                              "frac_of_mix_ceiling": achieved / MIX_CEILING_GBS},
                 "clocks": clk.summary(),
                 "e2e": {"value": e2e_value, "unit": "blocks/s", "h2d_bytes_per_step": N_IMG * H * W,
                         "d2h_bytes_per_step": nblocks * 1024, "steps": e2e_steps,
-                        "path": "pinned host images -> forward_host (2-stream chunked H2D/kernel/D2H) -> pinned host coef",
+                        "path": "pinned host images -> dct16a_forward_host (C entry: chunked H2D / forward / D2H "
+                                "on two library streams) -> pinned host coef",
                         "host_matches_device": bool(ok)},
-                "gpu_launches": args.steps}
+                "gpu_launches": args.steps,
+                "configs": configs}
         if world == 1 and not args.no_cpu_baseline:
             workers = host_cores()
-            # all 4096 images: ~25 CPU-s of oracle work, ~2 s of wall time on a 16-core host
-            n_s = int(os.environ.get("DCT16A_ORACLE_IMAGES", "4096"))
-            r, cpu, wall = oracle_rate(n_s, workers)
-            line["cpu_baseline"] = {"value": r, "unit": "blocks/s", "cores": workers, "kind": "oracle",
+            cpu = cpu_model()
+            n_s = int(os.environ.get("DCT16A_ORACLE_IMAGES", "1024"))
+            imgs = synth.batch_u8(range(n_s), H, W)
+            r, cs, wall = oracle_rate("cfg2", imgs, workers)
+            line["cpu_baseline"] = {"value": r, "unit": "blocks/s", "cores": workers, "cpu": cpu, "kind": "oracle",
                                     "sample": f"{n_s} of the 4096 config-2 images ({n_s * BLOCKS_PER_IMG} blocks), "
-                                              f"oracle.codec.forward, {cpu:.1f} CPU-s over {wall:.1f} s wall"}
+                                              f"oracle.codec.forward, {cs:.1f} CPU-s over {wall:.1f} s wall"}
+            for name, what, unit in (("cfg3", "24 config-3 frames", "blocks/s"),
+                                     ("cfg4", "6 distinct config-4 frames", "blocks/s"),
+                                     ("cfg5", "16 256x256 crops of 4 config-5 images x r = 1..256", "block-evaluations/s")):
+                if samples.get(name) is None:
+                    continue
+                r, cs, wall = oracle_rate(name, samples[name], workers)
+                configs[name]["oracle"] = {"value": r, "unit": unit, "cores": min(workers, len(samples[name])),
+                                           "cpu": cpu, "kind": "oracle",
+                                           "sample": f"{what}, oracle.codec as it stands, {wall:.1f} s wall"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-    del np
 
 
 def main():
@@ -299,11 +485,12 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--cfg-steps", type=int, default=10, help="timed steps of the config 3/4/5 legs")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--headline-only", action="store_true", help="config 2 only (skip the config 3/4/5 legs)")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -11,7 +11,12 @@
  * never synchronises the stream.  Constants live in __constant__ memory; the
  * only state is the dynamic tile schedulers' counters (static __device__
  * arrays of 64 slots per kernel family, taken round-robin by successive calls
- * and reset by each launch's last warp: see dct16a_forward and dct16a_codec).
+ * and reset by each launch's last warp) and, on the host, one completion event
+ * per slot: a call whose slot was last used by a launch on ANOTHER stream that
+ * may still be running makes its own stream wait for that launch first
+ * (cudaStreamWaitEvent), so concurrent launches never share a counter, however
+ * many are in flight.  A call made while its stream is being captured into a
+ * CUDA graph takes no slot (static tile schedule: replays may overlap freely).
  * Calls are thread-safe and re-entrant.
  *
  * Errors: every function validates all arguments synchronously before any
@@ -90,13 +95,11 @@ typedef struct dct16a_quant {
  * dct16a_forward — Z = T·X·Tᵀ for every block (separable
  * row/column passes of the Eq. (1) network as in PAPER.md:1072-1090).
  *   src  : image batch laid out as described by *desc (uint8 or int16).
- *   coef : int32 output, batch·BY·BX·256 entries, block-major (see above).
+ *   coef : int32 output, batch·BY·BX·256 entries, block-major (see above);
+ *          must not overlap src (DCT16A_EDOMAIN).
  * Integer-exact.  |Z| <= 65280 (8-bit) / 261888 (10-bit).
- * Scheduling: the kernel hands out tiles from one of 64 device-side counters
- * used round-robin by successive calls (a compact write window);
- * at most 64 dct16a_forward / dct16a_forward16 launches may be executing at
- * the same time (on any streams) per device.  A launch captured in a CUDA
- * graph keeps its counter: replays of one graph must not overlap in time.
+ * Scheduling: the kernel hands out tiles from a device-side counter (a
+ * compact write window; slot rules in the file header).
  */
 DCT16A_API int dct16a_forward(const void* src, const dct16a_desc* desc,
                               int32_t* coef, void* stream);
@@ -157,14 +160,11 @@ DCT16A_API int dct16a_psnr(const void* ref, const void* test, const dct16a_desc*
  * dct16a_psnr.
  *   recon : optional pixels out (may be NULL: nothing is written), in the
  *           layout, pitch, image stride and type of *desc — one descriptor
- *           describes both src and recon; must not overlap src.
+ *           describes both src and recon; its byte range must not intersect
+ *           src's (DCT16A_EDOMAIN).
  *   sse   : uint64 out [batch] (exact; overwritten, not accumulated).
  *   psnr  : optional float64 out [batch] (may be NULL).
- * Scheduling: the default kernels hand out tiles from one of 64 device-side
- * counters per kernel, used round-robin by successive calls (as
- * dct16a_forward); at most 64 dct16a_codec / dct16a_codec_allreduce launches
- * may be executing at the same time (on any streams) per device, and replays
- * of one captured CUDA graph must not overlap in time.
+ * Scheduling: as dct16a_forward (file header).
  */
 DCT16A_API int dct16a_codec(const void* src, const dct16a_desc* desc,
                             const dct16a_quant* quant, void* recon,
@@ -190,6 +190,21 @@ DCT16A_API int dct16a_codec(const void* src, const dct16a_desc* desc,
 DCT16A_API int dct16a_codec_allreduce(const void* src, const dct16a_desc* desc, const dct16a_quant* quant,
                                       void* recon, uint64_t* const* sse_peers, int32_t n_peers,
                                       int64_t frame_offset, void* stream);
+
+/*
+ * dct16a_codec_allreduce_multicast — dct16a_codec_allreduce through an NVLS
+ * multicast address: sse_multicast maps the per-frame SSE
+ * vectors of every GPU of the group (e.g. torch symmetric memory
+ * multicast_ptr on an NVSwitch system); each image's SSE is added with one
+ * multimem.red.relaxed.sys.global.add.u64, which the switch applies to every
+ * GPU's copy.  Same ordering contract as dct16a_codec_allreduce (zero and
+ * synchronise every rank before, synchronise after).  Passing an address that
+ * is not a multicast mapping is undefined (the instruction faults).
+ * Errors as dct16a_codec_allreduce.
+ */
+DCT16A_API int dct16a_codec_allreduce_multicast(const void* src, const dct16a_desc* desc, const dct16a_quant* quant,
+                                                void* recon, uint64_t* sse_multicast, int64_t frame_offset,
+                                                void* stream);
 
 /*
  * dct16a_ssim — mean SSIM per image (Wang et al. 2004):
@@ -221,6 +236,46 @@ DCT16A_API int dct16a_zonal_sweep(const void* src, const dct16a_desc* desc, int3
                                   int32_t r_count, uint64_t* sse, double* psnr, void* stream);
 
 /*
+ * dct16a_sse_psnr — the PSNR finaliser of the path (PAPER.md:906-910,
+ * readings A7/A8) on its own: for `count` per-image SSE values of images
+ * described by *desc (peak 2^b - 1, P = valid_height·width pixels each;
+ * desc->batch is not used), writes
+ *   psnr[i]     = 10·log10(peak²·P/sse[i]), +INFINITY for 0     (may be NULL),
+ *   *sse_total  = Σ sse[i], exact                              (may be NULL),
+ *   *psnr_total = 10·log10(peak²·P·count/Σ sse[i])             (may be NULL):
+ * config 4's global PSNR over all frames after the SSE all-reduce.
+ *   sse : DEVICE uint64 [count]; outputs are DEVICE pointers, 8-byte aligned.
+ * Errors: DCT16A_ESHAPE for count outside [1, 2^31).
+ */
+DCT16A_API int dct16a_sse_psnr(const uint64_t* sse, int64_t count, const dct16a_desc* desc, double* psnr,
+                               uint64_t* sse_total, double* psnr_total, void* stream);
+
+/*
+ * dct16a_forward_host — dct16a_forward end to end from HOST memory: the
+ * images are read from host_src (laid out as *desc describes) and Z is
+ * written to host_coef (int32, block-major, batch·BY·BX·256 entries).  The
+ * batch is cut into chunks of whole images; chunk i is copied host->device
+ * (one cudaMemcpyAsync), transformed, and copied device->host (one
+ * cudaMemcpyAsync) on the i-th of two library-owned streams (created once per
+ * device, joined to `stream` by events), so copies in both directions overlap
+ * each other and the transform.  Asynchronous on `stream` like every entry:
+ * synchronise it before reading host_coef.  host_src / host_coef should be
+ * page-locked (cudaHostAlloc / pinned torch tensors) for the copies to overlap.
+ *   workspace       : DEVICE scratch, 1024-byte aligned, owned by the caller,
+ *                     holding two chunk slots (input + coefficients);
+ *   workspace_bytes : its size; the chunk is the largest number of images
+ *                     whose two slots fit.
+ * Errors: DCT16A_EDOMAIN if the workspace holds less than one image per slot
+ * (see dct16a_forward_host_workspace); DCT16A_EALIGN for a misaligned workspace.
+ */
+DCT16A_API int dct16a_forward_host(const void* host_src, const dct16a_desc* desc, int32_t* host_coef,
+                                   void* workspace, int64_t workspace_bytes, void* stream);
+
+/* Workspace bytes dct16a_forward_host needs for chunks of `chunk_images`
+ * images (negative DCT16A_E* code on a bad descriptor or chunk_images < 1). */
+DCT16A_API int64_t dct16a_forward_host_workspace(const dct16a_desc* desc, int32_t chunk_images);
+
+/*
  * dct16a_set_option / dct16a_get_option — process-wide knobs for tuning and
  * cross-checking; they never change results (every kernel choice computes the
  * same bytes).  Initial values come from the environment variables named
@@ -228,10 +283,15 @@ DCT16A_API int dct16a_zonal_sweep(const void* src, const dct16a_desc* desc, int3
  *   DCT16A_OPT_CODEC_PATH (env DCT16A_CODEC_PATH): fused-codec kernel choice,
  *     0 = automatic (default): zonal 8-bit with r <= 36 on the band-pruned
  *         warp-per-tile kernel, everything else on the warp-per-block-pair kernel;
- *     1 = zonal on the generic kernel; 2 = always the warp-per-block-pair kernel;
- *     3 = zonal 8-bit with r <= 36 on the thread-per-block kernel.
+ *     2 = always the warp-per-block-pair kernel.
+ *     (Libraries built with -DDCT16A_EXPERIMENTS also take 1 = zonal on the
+ *     generic kernel and 3 = zonal 8-bit r <= 36 on the thread-per-block kernel.)
  *   DCT16A_OPT_FWD_STORE (env DCT16A_FWD_STORE): output path of the forward
- *     kernel, -1 = default, 0..5 = the variants of profiles/r01_fwd_store_modes.md.
+ *     kernel, -1 = default (5 for 8-bit, 3 for 10-bit), 3 = 8 KB TMA stores,
+ *     5 = one 32 KB TMA store per tile (experiment builds: 0..7, the variants
+ *     of profiles/r01_fwd_store_modes.md).
+ * A value the library was not built with returns DCT16A_EDOMAIN (from the
+ * environment it is ignored).
  */
 #define DCT16A_OPT_CODEC_PATH 1
 #define DCT16A_OPT_FWD_STORE  2

@@ -9,9 +9,10 @@ memory, streams and process groups only.
 from __future__ import annotations
 
 from ._lib import (OPT_CODEC_PATH, OPT_FWD_STORE, UNIFORM, ZONAL, Dct16aError, Desc, Quant,  # noqa: F401
-                   dct16a_codec, dct16a_codec_allreduce, dct16a_forward, dct16a_forward16, dct16a_get_option, dct16a_inverse, dct16a_last_error,
-                   dct16a_psnr, dct16a_quantize, dct16a_set_option, dct16a_ssim, dct16a_version, dct16a_zonal_sweep, desc_of, lib,
-                   make_desc, make_quant)
+                   dct16a_codec, dct16a_codec_allreduce, dct16a_forward, dct16a_forward16, dct16a_forward_host,
+                   dct16a_forward_host_workspace, dct16a_get_option, dct16a_inverse, dct16a_last_error, dct16a_psnr,
+                   dct16a_quantize, dct16a_set_option, dct16a_sse_psnr, dct16a_ssim, dct16a_version, dct16a_zonal_sweep,
+                   desc_of, lib, make_desc, make_quant)
 
 __version__ = "0.1.0"
 
@@ -83,39 +84,24 @@ def zonal_sweep(images, r_first=1, r_count=256, valid_height=None, stream=None):
     return sse, psnr
 
 
-def forward_host(host_images, host_coef, chunk_images=256, device=None, bufs=None):
+def forward_host(host_images, host_coef, chunk_images=256, device=None, workspace=None, stream=None):
     """End-to-end forward transform from PINNED host images to PINNED host
-    coefficients: the batch is cut into chunks; chunk i's host->device copy,
-    transform and device->host copy run on stream i % 2, so copies in both
-    directions overlap each other and the transform.  Returns the device
-    buffers for reuse (pass them back as `bufs`).
+    coefficients through the C entry dct16a_forward_host: chunks of
+    `chunk_images` images alternate between two library streams, so the
+    host->device copies, the transform and the device->host copies overlap.
+    Returns the device workspace for reuse (pass it back as `workspace`).
 
     host_images: (batch, H, W) uint8/int16 pinned CPU tensor.
     host_coef:   (batch·H/16·W/16, 16, 16) int32 pinned CPU tensor.
     """
     import torch
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
-    n, h, w = host_images.shape
-    per_img = (h // 16) * (w // 16)
-    c = max(1, min(chunk_images, n))
-    if bufs is None:
-        streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
-        xin = [torch.empty((c, h, w), dtype=host_images.dtype, device=dev) for _ in range(2)]
-        cout = [torch.empty((c * per_img, 16, 16), dtype=torch.int32, device=dev) for _ in range(2)]
-        bufs = (streams, xin, cout)
-    streams, xin, cout = bufs
-    cur = torch.cuda.current_stream(dev)
-    for s in streams:
-        s.wait_stream(cur)
-    for i, s0 in enumerate(range(0, n, c)):
-        m = min(c, n - s0)
-        st = streams[i & 1]
-        with torch.cuda.stream(st):
-            xi = xin[i & 1][:m]
-            ci = cout[i & 1][:m * per_img]
-            xi.copy_(host_images[s0:s0 + m], non_blocking=True)
-            dct16a_forward(xi, ci, desc_of(xi), st)
-            host_coef[s0 * per_img:(s0 + m) * per_img].copy_(ci, non_blocking=True)
-    for s in streams:
-        cur.wait_stream(s)
-    return bufs
+    d = desc_of(host_images)
+    need = dct16a_forward_host_workspace(d, chunk_images)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)   # caching allocator: 512-B..2 MB aligned
+        if workspace.data_ptr() % 1024:
+            workspace = torch.empty(need + 1024, dtype=torch.uint8, device=dev)
+            workspace = workspace[(-workspace.data_ptr()) % 1024:][:need]
+    dct16a_forward_host(host_images, host_coef, workspace, d, stream)
+    return workspace

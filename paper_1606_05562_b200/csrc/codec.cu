@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(256) quantize_kernel(const int4* __restrict__ 
 
 namespace {
 
+#ifdef DCT16A_EXPERIMENTS   // the generic codec kernel reads rows straight from global memory
 __device__ __forceinline__ void load_row(const uint8_t* p, int elem, int32_t (&x)[16]) {
     if (elem == 1) {
         const uint4 v = __ldcs(reinterpret_cast<const uint4*>(p));
@@ -87,6 +88,7 @@ __device__ __forceinline__ void load_row(const uint8_t* p, int elem, int32_t (&x
         for (int j = 0; j < 16; ++j) x[j] = static_cast<int16_t>((w[j >> 1] >> (16 * (j & 1))) & 0xFFFF);
     }
 }
+#endif
 
 __device__ __forceinline__ void store_row(uint8_t* p, int elem, const int (&v)[16]) {
     if (elem == 1) {
@@ -231,6 +233,8 @@ __global__ void __launch_bounds__(kInvWarps * 32) inverse_kernel(const int32_t* 
     }
 }
 
+#ifdef DCT16A_EXPERIMENTS
+// Experiment build only (codec path 1, tools/variants.py).
 // ------------------------------------------------------- fused codec (K2/K3)
 struct CodecParams {
     int PX;                  // block pairs per strip = ceil(BX / 2)
@@ -345,6 +349,8 @@ __global__ void __launch_bounds__(kCodecWarps * 32) codec_kernel(const uint8_t* 
     if (lane == 0 && acc) atomicAdd(sse + cur_n, acc);
 }
 
+#endif  // DCT16A_EXPERIMENTS
+
 // ------------------------------------------------------------------ K6
 __global__ void sse_kernel(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b,
                            unsigned long long* sse, const Geom g) {
@@ -405,6 +411,36 @@ int launch_psnr_finish(const Geom& g, long long count, uint64_t* sse, double* ps
     return static_cast<int>(cudaGetLastError());
 }
 
+// The exact total of `n` SSE values and the PSNR of the whole set (one CTA:
+// config 4's global PSNR after the SSE all-reduce, reading A8).
+__global__ void __launch_bounds__(1024) sse_total_kernel(const unsigned long long* sse, long long n,
+                                                         unsigned long long* total, double* psnr_total,
+                                                         double peak2P) {
+    __shared__ unsigned long long ws[32];
+    unsigned long long acc = 0;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) acc += sse[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += ws[w];
+        if (total) *total = s;
+        if (psnr_total) *psnr_total = s == 0 ? INFINITY : 10.0 * log10(peak2P * static_cast<double>(n) / static_cast<double>(s));
+    }
+}
+
+int launch_sse_total(const Geom& g, long long count, const uint64_t* sse, uint64_t* total, double* psnr_total,
+                     cudaStream_t st) {
+    if (!total && !psnr_total) return 0;
+    const double peak = static_cast<double>((1 << g.bits) - 1);
+    const double P = static_cast<double>(g.VH) * g.W;
+    sse_total_kernel<<<1, 1024, 0, st>>>(reinterpret_cast<const unsigned long long*>(sse), count,
+                                        reinterpret_cast<unsigned long long*>(total), psnr_total, peak * peak * P);
+    return static_cast<int>(cudaGetLastError());
+}
+
 namespace {
 int finish_psnr(const Geom& g, uint64_t* sse, double* psnr, cudaStream_t st) {
     return launch_psnr_finish(g, g.N, sse, psnr, st);
@@ -449,6 +485,7 @@ int launch_psnr(const void* ref, const void* test, const Geom& g, uint64_t* sse,
     return finish_psnr(g, sse, psnr, st);
 }
 
+#ifdef DCT16A_EXPERIMENTS
 int launch_codec_generic(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse,
                          cudaStream_t st) {
     CodecParams cp;
@@ -466,26 +503,28 @@ int launch_codec_generic(const void* src, const Geom& g, const dct16a_quant& q, 
         cp);
     return static_cast<int>(cudaGetLastError());
 }
+#endif  // DCT16A_EXPERIMENTS
 
 // Kernel choice of the fused codec (option DCT16A_OPT_CODEC_PATH, include/dct16a.h):
 //   0 auto: zonal 8-bit with r <= 36 -> band-pruned warp kernel (zonal_band.cu),
 //           everything else -> warp-per-block-pair kernel (codec_warp.cu);
-//   1: zonal -> the generic kernel above (uniform stays on codec_warp.cu);
-//   2: always codec_warp.cu;
-//   3: zonal 8-bit with r <= 36 -> thread-per-block kernel (zonal_tpb.cu).
-// The four implementations are independent cross-checks of each other.
+//   2: always codec_warp.cu.
+// Experiment builds (-DDCT16A_EXPERIMENTS) add 1 (zonal on the generic kernel
+// above) and 3 (zonal 8-bit r <= 36 on the thread-per-block kernel,
+// zonal_tpb.cu).  Every path computes the same bytes.
 int launch_codec(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse,
                  double* psnr, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(uint64_t) * g.N, st);
     if (e) return static_cast<int>(e);
     const int path = get_option(DCT16A_OPT_CODEC_PATH);
-    int rc = 1;
-    if (q.mode == DCT16A_ZONAL && path == 0) rc = launch_zonal_band(src, g, q.r, recon, sse, st);
-    if (q.mode == DCT16A_ZONAL && path == 3) rc = launch_zonal_tpb(src, g, q.r, recon, sse, st);
-    if (rc == 1) {
-        if (q.mode == DCT16A_ZONAL && path == 1) rc = launch_codec_generic(src, g, q, recon, sse, st);
-        else rc = launch_codec_warp(src, g, q, recon, sse, st);
-    }
+    const bool zonal = q.mode == DCT16A_ZONAL;
+    int rc;
+    if (zonal && path == 0 && zonal_band_applies(g, q.r)) rc = launch_zonal_band(src, g, q.r, recon, sse, st);
+#ifdef DCT16A_EXPERIMENTS
+    else if (zonal && path == 3 && zonal_band_applies(g, q.r)) rc = launch_zonal_tpb(src, g, q.r, recon, sse, st);
+    else if (zonal && path == 1) rc = launch_codec_generic(src, g, q, recon, sse, st);
+#endif
+    else rc = launch_codec_warp(src, g, q, recon, sse, st);
     if (rc) return rc;
     return finish_psnr(g, sse, psnr, st);
 }

@@ -48,6 +48,7 @@
 #include "internal.h"
 #include "net16.cuh"
 #include "ptx.cuh"
+#include "sched.cuh"
 #include "quant.cuh"
 #include "tables.cuh"
 #include "tile128.cuh"
@@ -90,23 +91,19 @@ constexpr int kMaxPeers = 8;
 #define DCT16A_CW_CLAIM 4
 #endif
 constexpr int kWClaim = DCT16A_CW_CLAIM;   // consecutive tiles per claim
-// Dynamic tile scheduler (as in forward.cu / zonal_band.cu): runs of kWClaim
-// tiles claimed in increasing order from a global counter keep the tiles in
-// flight in one compact address window; 64 slots round-robin over launches,
-// reset by the last warp (at most 64 concurrent launches per device).
-constexpr int kWSchedSlots = 64;
-__device__ unsigned long long g_cw_sched[kWSchedSlots][2];
-// one host-side slot counter for every instantiation of the kernel (they share g_cw_sched)
-std::atomic<unsigned> g_cw_launch_seq{0};
+// Dynamic tile scheduler (sched.cuh, as in forward.cu / zonal_band.cu): runs of
+// kWClaim tiles claimed in increasing order from a global counter keep the
+// tiles in flight in one compact address window.
+__device__ unsigned long long g_cw_sched[kSchedSlots][2];
 
 struct WParams {
     int W, BX, BY, VH, tiles_per_strip, maxpix;
     long long n_tiles;
-    int slot, total_warps, claim;   // dynamic tile scheduler (claim = tiles per claim)
+    int slot, total_warps, claim;   // tile scheduler (sched.cuh; slot -1 = static), tiles per claim
     int has_recon;
     // fused SSE all-reduce (dct16a_codec_allreduce): every image's SSE is added
     // into sse_peers[q][frame_offset + n] of every peer q; n_peers = 0: local sse
-    int n_peers;
+    int n_peers, multicast;   // multicast: peers[0] is an NVLS multicast address
     long long frame_offset;
     unsigned long long* peers[kMaxPeers];
     // zonal
@@ -174,12 +171,19 @@ __device__ __noinline__ int32_t uniform_fix_call(float z, int32_t m, int step, i
 
 }  // namespace
 
-// Add one image's SSE: locally, or into every peer's vector over NVLink (system-
-// scope 64-bit atomics on peer-mapped memory: integer adds, order-independent,
-// so every rank ends with the exact per-frame sums — the path's all-reduce).
+// Add one image's SSE: locally, or into every rank's vector — with one
+// multimem.red on the NVLS multicast address (the NVSwitch applies the add to
+// every GPU's copy) or with system-scope 64-bit atomics on each peer-mapped
+// vector over NVLink.  Integer adds are order-independent, so every rank ends
+// with the exact per-frame sums: the path's all-reduce.
 __device__ __forceinline__ void flush_sse(unsigned long long* sse, const WParams& p, int n, unsigned long long v) {
     if (p.n_peers == 0) {
         atomicAdd(sse + n, v);
+        return;
+    }
+    if (p.multicast) {
+        asm volatile("multimem.red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p.peers[0] + p.frame_offset + n), "l"(v)
+                     : "memory");
         return;
     }
     for (int q = 0; q < p.n_peers; ++q) atomicAdd_system(p.peers[q] + p.frame_offset + n, v);
@@ -202,14 +206,15 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
     int4* coords = reinterpret_cast<int4*>(smem + kWWarps * Cfg::kWarpBytes + kWWarps * kWStages * 8) +
                    warp * kWStages;
     const uint64_t pol = policy_evict_first();
-    unsigned long long* sched = g_cw_sched[p.slot];
+    unsigned long long* sched = p.slot >= 0 ? g_cw_sched[p.slot] : nullptr;
+    Claims claims(sched, static_cast<long long>(blockIdx.x) * kWWarps + warp, static_cast<long long>(gridDim.x) * kWWarps);   // lane 0
 
     // lane 0: the claim in progress (tiles [next, end)) and its cursor
     long long next = 0, end = 0;
     TileCursor ic;
     auto issue_next = [&](int st) {   // claim the next tile, load it into stage st (lane 0)
         if (next == end) {
-            const long long first = static_cast<long long>(atomicAdd(&sched[0], 1ull)) * p.claim;
+            const long long first = claims.next() * p.claim;
             next = first;
             end = first < p.n_tiles ? min(first + p.claim, p.n_tiles) : first;
             if (first < p.n_tiles) ic.init(p, first);
@@ -450,11 +455,7 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
     if (lane == 0) {
         if (acc) flush_sse(sse, p, cur_n, acc);
         if (p.has_recon) bulk_wait<0>();
-        if (atomicAdd(&sched[1], 1ull) == static_cast<unsigned long long>(p.total_warps) - 1) {
-            // every warp has claimed past the end: reset the slot for a later launch
-            sched[0] = 0;
-            sched[1] = 0;
-        }
+        claims_done(sched, p.total_warps);   // every warp has claimed past the end
     }
 }
 
@@ -462,7 +463,7 @@ namespace {
 
 template <int ELEM, bool UNIFORM>
 int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse, cudaStream_t st,
-              uint64_t* const* peers = nullptr, int n_peers = 0, long long frame_offset = 0) {
+              uint64_t* const* peers = nullptr, int n_peers = 0, long long frame_offset = 0, int multicast = 0) {
     using Cfg = WCfg<ELEM, UNIFORM>;
     CUtensorMap tin, tout;
     const uint64_t dims[3] = {uint64_t(g.W), uint64_t(g.H), uint64_t(g.N)};
@@ -489,6 +490,7 @@ int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon
     p.n_tiles = static_cast<long long>(g.N) * g.BY * p.tiles_per_strip;
     p.has_recon = recon != nullptr;
     p.n_peers = n_peers;
+    p.multicast = multicast;
     p.frame_offset = frame_offset;
     for (int i = 0; i < n_peers; ++i) p.peers[i] = reinterpret_cast<unsigned long long*>(peers[i]);
     p.r = q.r;
@@ -525,8 +527,10 @@ int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon
     p.claim = static_cast<int>(std::min<long long>(kWClaim, std::max<long long>(1, p.n_tiles / (grid * kWWarps * 4))));
     const long long want = (p.n_tiles + kWWarps * p.claim - 1) / (kWWarps * p.claim);
     if (want < grid) grid = want;
-    p.slot = static_cast<int>(g_cw_launch_seq.fetch_add(1) % kWSchedSlots);
     p.total_warps = static_cast<int>(grid) * kWWarps;
+    SchedGuard guard(kSchedCodecWarp, st);
+    if (guard.error()) return guard.error();
+    p.slot = guard.slot();
     codec_warp_kernel<ELEM, UNIFORM><<<static_cast<unsigned>(grid), kWWarps * 32, Cfg::kSmem, st>>>(
         tin, tout, reinterpret_cast<unsigned long long*>(sse), p);
     return static_cast<int>(cudaGetLastError());
@@ -542,13 +546,14 @@ int launch_codec_warp(const void* src, const Geom& g, const dct16a_quant& q, voi
 }
 
 int launch_codec_allreduce(const void* src, const Geom& g, const dct16a_quant& q, void* recon,
-                           uint64_t* const* peers, int n_peers, long long frame_offset, cudaStream_t st) {
+                           uint64_t* const* peers, int n_peers, long long frame_offset, int multicast,
+                           cudaStream_t st) {
     const bool uni = q.mode == DCT16A_UNIFORM;
     if (g.elem == 1)
-        return uni ? launch_cw<1, true>(src, g, q, recon, nullptr, st, peers, n_peers, frame_offset)
-                   : launch_cw<1, false>(src, g, q, recon, nullptr, st, peers, n_peers, frame_offset);
-    return uni ? launch_cw<2, true>(src, g, q, recon, nullptr, st, peers, n_peers, frame_offset)
-               : launch_cw<2, false>(src, g, q, recon, nullptr, st, peers, n_peers, frame_offset);
+        return uni ? launch_cw<1, true>(src, g, q, recon, nullptr, st, peers, n_peers, frame_offset, multicast)
+                   : launch_cw<1, false>(src, g, q, recon, nullptr, st, peers, n_peers, frame_offset, multicast);
+    return uni ? launch_cw<2, true>(src, g, q, recon, nullptr, st, peers, n_peers, frame_offset, multicast)
+               : launch_cw<2, false>(src, g, q, recon, nullptr, st, peers, n_peers, frame_offset, multicast);
 }
 
 }  // namespace dct16a

@@ -32,6 +32,7 @@
 #include "internal.h"
 #include "net16.cuh"
 #include "ptx.cuh"
+#include "sched.cuh"
 
 namespace dct16a {
 namespace {
@@ -73,23 +74,17 @@ struct FwdCfg {
 struct FwdParams {
     int W, BX, BY, tiles_per_strip, box_w;
     long long n_tiles;
-    int slot;            // dynamic scheduler slot (DCT16A_FWD_DYN)
+    int slot;            // tile-scheduler slot, -1 = static schedule (sched.cuh)
     int total_warps;
 };
 
-#ifndef DCT16A_FWD_DYN
-#define DCT16A_FWD_DYN 1
-#endif
-// Dynamic tile scheduler: warps claim tiles in increasing order from a global
-// counter, so the tiles in flight form one compact address window (the static
-// stride schedule lets warps drift apart and spreads the concurrent writes over
-// many DRAM pages: 5.6 vs 6.2 TB/s for the same byte mix in
-// tools/dbg/mix_dynamic.cu).  64 slots are used round-robin by successive
-// launches; the last warp of a launch resets its slot.
-constexpr int kSchedSlots = 64;
+// Dynamic tile scheduler (sched.cuh): warps claim tiles in increasing order
+// from a global counter, so the tiles in flight form one compact address window
+// (the static stride schedule lets warps drift apart and spreads the concurrent
+// writes over many DRAM pages: 5.6 vs 6.2 TB/s for the same byte mix in
+// tools/dbg/mix_dynamic.cu).  A launch captured into a CUDA graph uses the
+// static schedule.
 __device__ unsigned long long g_fwd_sched[kSchedSlots][2];
-// one host-side slot counter for every instantiation of the kernel (they share g_fwd_sched)
-std::atomic<unsigned> g_fwd_launch_seq{0};
 
 // Pad the dynamic smem base to 1024 B (128-byte swizzle atoms) while keeping
 // the pointer derived from the __shared__ array, so the compiler emits LDS/STS.
@@ -135,7 +130,8 @@ __global__ void __launch_bounds__(FwdCfg<ELEM, SM>::kWarps * 32, FwdCfg<ELEM, SM
     const long long gw = static_cast<long long>(blockIdx.x) * Cfg::kWarps + warp;
     const long long nw = static_cast<long long>(gridDim.x) * Cfg::kWarps;
     const uint64_t pol = policy_evict_first();
-    unsigned long long* sched = g_fwd_sched[p.slot];
+    unsigned long long* sched = p.slot >= 0 ? g_fwd_sched[p.slot] : nullptr;
+    Claims claims(sched, gw, nw);   // lane 0 only
 
     // tile of pipeline stage s (lane 0 holds the truth; broadcast when used)
     long long ring[kStages];
@@ -145,7 +141,7 @@ __global__ void __launch_bounds__(FwdCfg<ELEM, SM>::kWarps * 32, FwdCfg<ELEM, SM
         prefetch_tmap(&tin);
         prefetch_tmap(&tout);
         for (int s = 0; s < kStages; ++s) {
-            const long long t = DCT16A_FWD_DYN ? static_cast<long long>(atomicAdd(&sched[0], 1ull)) : gw + s * nw;
+            const long long t = claims.next();
             ring[s] = t;
             if (t < p.n_tiles) issue_tile<ELEM>(&tin, p, t, wbase + s * Cfg::kStageBytes, &bars[s], pol);
         }
@@ -217,7 +213,7 @@ __global__ void __launch_bounds__(FwdCfg<ELEM, SM>::kWarps * 32, FwdCfg<ELEM, SM
         __syncwarp();
         // stage s fully consumed by every lane: refill it with the tile kStages ahead
         if (lane == 0) {
-            const long long nt = DCT16A_FWD_DYN ? static_cast<long long>(atomicAdd(&sched[0], 1ull)) : tix + kStages * nw;
+            const long long nt = claims.next();
 #pragma unroll
             for (int q = 0; q < kStages; ++q)
                 if (q == s) ring[q] = nt;
@@ -330,11 +326,7 @@ __global__ void __launch_bounds__(FwdCfg<ELEM, SM>::kWarps * 32, FwdCfg<ELEM, SM
     }
     if (lane == 0) {
         bulk_wait<0>();
-        if (DCT16A_FWD_DYN && atomicAdd(&sched[1], 1ull) == static_cast<unsigned long long>(p.total_warps) - 1) {
-            // every warp has claimed past the end: reset the slot for a later launch
-            sched[0] = 0;
-            sched[1] = 0;
-        }
+        claims_done(sched, p.total_warps);   // every warp has claimed past the end
     }
 }
 
@@ -383,8 +375,10 @@ int launch_fwd_t(const void* src, const Geom& g, int32_t* coef, cudaStream_t st)
     const long long want = (p.n_tiles + Cfg::kWarps - 1) / Cfg::kWarps;
     long long grid = static_cast<long long>(num_sms()) * Cfg::kMinCtas;
     if (want < grid) grid = want;
-    p.slot = static_cast<int>(g_fwd_launch_seq.fetch_add(1) % kSchedSlots);
     p.total_warps = static_cast<int>(grid) * Cfg::kWarps;
+    SchedGuard guard(kSchedForward, st);
+    if (guard.error()) return guard.error();
+    p.slot = guard.slot();
     fwd_kernel<ELEM, SM><<<static_cast<unsigned>(grid), Cfg::kWarps * 32, Cfg::kSmem, st>>>(tin, tout, coef, p);
     return static_cast<int>(cudaGetLastError());
 }
@@ -402,14 +396,18 @@ int store_mode(int elem) {
 template <int ELEM>
 int launch_fwd_e(const void* src, const Geom& g, int32_t* coef, cudaStream_t st) {
     switch (store_mode(ELEM)) {
+        case 3: return launch_fwd_t<ELEM, 3>(src, g, coef, st);
+        case 5: return launch_fwd_t<ELEM, 5>(src, g, coef, st);
+#ifdef DCT16A_EXPERIMENTS
+        // the store-path experiments of profiles/r01_fwd_store_modes.md (tools/variants.py)
+        case 0: return launch_fwd_t<ELEM, 0>(src, g, coef, st);
         case 1: return launch_fwd_t<ELEM, 1>(src, g, coef, st);
         case 2: return launch_fwd_t<ELEM, 2>(src, g, coef, st);
-        case 3: return launch_fwd_t<ELEM, 3>(src, g, coef, st);
         case 4: return launch_fwd_t<ELEM, 4>(src, g, coef, st);
-        case 5: return launch_fwd_t<ELEM, 5>(src, g, coef, st);
         case 6: return launch_fwd_t<ELEM, 6>(src, g, coef, st);
         case 7: return launch_fwd_t<ELEM, 7>(src, g, coef, st);
-        default: return launch_fwd_t<ELEM, 0>(src, g, coef, st);
+#endif
+        default: return DCT16A_EDOMAIN;   // dct16a_set_option admits only the built modes
     }
 }
 

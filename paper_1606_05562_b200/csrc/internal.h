@@ -43,10 +43,15 @@ int launch_psnr(const void* ref, const void* test, const Geom& g, uint64_t* sse,
                 cudaStream_t st);
 int launch_codec(const void* src, const Geom& g, const dct16a_quant& q, void* recon,
                  uint64_t* sse, double* psnr, cudaStream_t st);
-// thread-per-block zonal codec for 8-bit and small bands; returns 1 if not applicable
-int launch_zonal_tpb(const void* src, const Geom& g, int r, void* recon, uint64_t* sse, cudaStream_t st);
-int launch_zonal_band(const void* src, const Geom& g, int r, void* recon, uint64_t* sse, cudaStream_t st);
+// Smallest anti-diagonal band k + l <= d holding the first r zig-zag positions.
 int zonal_band(int r);
+// Whether the band-pruned zonal kernel (zonal_band.cu) covers a case.
+bool zonal_band_applies(const Geom& g, int r);
+int launch_zonal_band(const void* src, const Geom& g, int r, void* recon, uint64_t* sse, cudaStream_t st);
+#ifdef DCT16A_EXPERIMENTS
+// thread-per-block zonal codec (codec path 3), same applicability as the band kernel
+int launch_zonal_tpb(const void* src, const Geom& g, int r, void* recon, uint64_t* sse, cudaStream_t st);
+#endif
 // warp-per-block-pair codec (uniform, and zonal cases zonal_tpb does not take)
 int launch_codec_warp(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse,
                       cudaStream_t st);
@@ -56,10 +61,38 @@ int launch_ssim(const void* ref, const void* test, const Geom& g, double* ssim, 
 int launch_sweep(const void* src, const Geom& g, int r_first, int r_count, uint64_t* sse, double* psnr,
                  cudaStream_t st);
 int launch_psnr_finish(const Geom& g, long long count, uint64_t* sse, double* psnr, cudaStream_t st);
+// exact sum of `count` SSE values and the PSNR of the whole set (P·count pixels)
+int launch_sse_total(const Geom& g, long long count, const uint64_t* sse, uint64_t* total, double* psnr_total,
+                     cudaStream_t st);
 // fused codec + SSE all-reduce over peer memory (codec_warp.cu)
 int launch_codec_allreduce(const void* src, const Geom& g, const dct16a_quant& q, void* recon,
-                           uint64_t* const* peers, int n_peers, long long frame_offset, cudaStream_t st);
+                           uint64_t* const* peers, int n_peers, long long frame_offset, int multicast,
+                           cudaStream_t st);
 // library options (dct16a_set_option); read by the launchers
 int get_option(int option);
+
+// Host side of the tile schedulers (sched.cuh).  A launcher holds one guard
+// around its kernel launch: the guard gives the launch a counter slot of its
+// kernel family that no unfinished launch on another stream still uses (it
+// makes `st` wait on the slot's previous launch when that one may still be
+// running), records the slot's completion event after the launch and keeps the
+// family's slot table locked in between.  A launch being captured into a CUDA
+// graph gets slot -1: the static schedule, so overlapping replays of one graph
+// are safe.
+enum SchedFamily { kSchedForward = 0, kSchedBand = 1, kSchedCodecWarp = 2, kSchedFamilies = 3 };
+class SchedGuard {
+  public:
+    SchedGuard(int family, cudaStream_t st);
+    ~SchedGuard();
+    SchedGuard(const SchedGuard&) = delete;
+    SchedGuard& operator=(const SchedGuard&) = delete;
+    int slot() const { return slot_; }   // -1: static schedule
+    int error() const { return err_; }   // cudaError_t of the slot hand-over (0 = fine)
+
+  private:
+    void* state_ = nullptr;
+    cudaStream_t st_;
+    int slot_ = -1, err_ = 0;
+};
 
 }  // namespace dct16a

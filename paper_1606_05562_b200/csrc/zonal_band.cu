@@ -46,6 +46,7 @@
 #include "internal.h"
 #include "net16.cuh"
 #include "ptx.cuh"
+#include "sched.cuh"
 #include "quant.cuh"
 #include "tables.cuh"
 #include "tile128.cuh"
@@ -98,18 +99,13 @@ struct BParams {
     long long n_tiles;
     int r;
     int has_recon;
-    int slot, total_warps, claim;   // dynamic tile scheduler (claim = tiles per claim)
+    int slot, total_warps, claim;   // tile scheduler (sched.cuh; slot -1 = static), tiles per claim
 };
 
-// Dynamic tile scheduler (as the forward kernel's, forward.cu): warps claim runs
+// Dynamic tile scheduler (sched.cuh, as the forward kernel's): warps claim runs
 // of kBClaim consecutive tiles in increasing order from a global counter, so the
-// tiles in flight form one compact address window; 64 slots are used
-// round-robin by successive launches and the last warp of a launch resets its
-// slot (at most 64 concurrent launches per device).
-constexpr int kBSchedSlots = 64;
-__device__ unsigned long long g_zb_sched[kBSchedSlots][2];
-// one host-side slot counter for every instantiation of the kernel (they share g_zb_sched)
-std::atomic<unsigned> g_zb_launch_seq{0};
+// tiles in flight form one compact address window.
+__device__ unsigned long long g_zb_sched[kSchedSlots][2];
 
 }  // namespace
 
@@ -129,7 +125,8 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
     int4* coords = reinterpret_cast<int4*>(smem + kBWarps * (kBWarpBytes + kBXpose) + kBWarps * kBStages * 8) +
                    warp * kBStages;
     const uint64_t pol = policy_evict_first();
-    unsigned long long* sched = g_zb_sched[p.slot];
+    unsigned long long* sched = p.slot >= 0 ? g_zb_sched[p.slot] : nullptr;
+    Claims claims(sched, static_cast<long long>(blockIdx.x) * kBWarps + warp, static_cast<long long>(gridDim.x) * kBWarps);   // lane 0
 
     // lane 0: the claim in progress (tiles [next, end)) and its cursor
     long long next = 0, end = 0;
@@ -137,7 +134,7 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
     // claim the next tile and issue its load into stage `st` (lane 0 only)
     auto issue_next = [&](int st) {
         if (next == end) {
-            const long long first = static_cast<long long>(atomicAdd(&sched[0], 1ull)) * p.claim;
+            const long long first = claims.next() * p.claim;
             next = first;
             end = first < p.n_tiles ? min(first + p.claim, p.n_tiles) : first;
             if (first < p.n_tiles) ic.init(p, first);
@@ -322,11 +319,7 @@ __global__ void __launch_bounds__(kBWarps * 32, DCT16A_ZB_CTAS)
     if (lane == 0) {
         if (acc) atomicAdd(sse + cur_n, acc);
         if (p.has_recon) bulk_wait<0>();
-        if (atomicAdd(&sched[1], 1ull) == static_cast<unsigned long long>(p.total_warps) - 1) {
-            // every warp has claimed past the end: reset the slot for a later launch
-            sched[0] = 0;
-            sched[1] = 0;
-        }
+        claims_done(sched, p.total_warps);   // every warp has claimed past the end
     }
 }
 
@@ -364,8 +357,10 @@ int launch_zb(const void* src, const Geom& g, int r, void* recon, uint64_t* sse,
     p.claim = static_cast<int>(std::min<long long>(kBClaim, std::max<long long>(1, p.n_tiles / (grid * kBWarps * 4))));
     const long long want = (p.n_tiles + kBWarps * p.claim - 1) / (kBWarps * p.claim);
     if (want < grid) grid = want;
-    p.slot = static_cast<int>(g_zb_launch_seq.fetch_add(1) % kBSchedSlots);
     p.total_warps = static_cast<int>(grid) * kBWarps;
+    SchedGuard guard(kSchedBand, st);
+    if (guard.error()) return guard.error();
+    p.slot = guard.slot();
     zband_kernel<BAND><<<static_cast<unsigned>(grid), kBWarps * 32, kBSmem, st>>>(
         tin, tout, reinterpret_cast<unsigned long long*>(sse), p);
     return static_cast<int>(cudaGetLastError());
@@ -373,14 +368,22 @@ int launch_zb(const void* src, const Geom& g, int r, void* recon, uint64_t* sse,
 
 }  // namespace
 
-// Returns 1 if the band kernel does not cover this case (10-bit, or r > 36).
+// Smallest anti-diagonal band holding the first r zig-zag positions.
+int zonal_band(int r) {
+    int d = 0;
+    while ((d + 1) * (d + 2) / 2 < r) ++d;   // cells with k + l <= d: (d+1)(d+2)/2 (d <= 15)
+    return d;
+}
+
+bool zonal_band_applies(const Geom& g, int r) { return g.elem == 1 && zonal_band(r) <= 7; }
+
+// Callers check zonal_band_applies first (8-bit, r <= 36).
 int launch_zonal_band(const void* src, const Geom& g, int r, void* recon, uint64_t* sse, cudaStream_t st) {
-    if (g.elem != 1) return 1;
     const int band = zonal_band(r);
+    if (g.elem != 1 || band > 7) return DCT16A_EDOMAIN;
     if (band <= 3) return launch_zb<3>(src, g, r, recon, sse, st);
     if (band <= 5) return launch_zb<5>(src, g, r, recon, sse, st);
-    if (band <= 7) return launch_zb<7>(src, g, r, recon, sse, st);
-    return 1;
+    return launch_zb<7>(src, g, r, recon, sse, st);
 }
 
 }  // namespace dct16a

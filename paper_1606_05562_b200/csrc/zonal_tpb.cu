@@ -19,6 +19,10 @@
 // * SSE: per 4 pixels one vabsdiff4 + one dp4a against the original bytes.
 // * Data: TMA strip-tile loads into a 3-stage per-warp ring; the reconstruction
 //   overwrites the tile in place and leaves by TMA tensor store.
+// Experiment build only (-DDCT16A_EXPERIMENTS, codec path 3 via
+// dct16a_set_option; tools/variants.py): the product library ships the
+// warp-cooperative kernels (zonal_band.cu, codec_warp.cu) instead.
+#ifdef DCT16A_EXPERIMENTS
 #include <cuda.h>
 #include <stdint.h>
 
@@ -290,21 +294,14 @@ int launch_ztpb(const void* src, const Geom& g, int r, void* recon, uint64_t* ss
 
 }  // namespace
 
-// Smallest anti-diagonal band holding the first r zig-zag positions.
-int zonal_band(int r) {
-    int d = 0;
-    while ((d + 1) * (d + 2) / 2 < r) ++d;   // cells with k + l <= d: (d+1)(d+2)/2 (d <= 15)
-    return d;
-}
-
-// Returns 1 if the thread-per-block path does not cover this case.
+// Callers check zonal_band_applies first (8-bit, r <= 36).
 int launch_zonal_tpb(const void* src, const Geom& g, int r, void* recon, uint64_t* sse, cudaStream_t st) {
-    if (g.elem != 1) return 1;
     const int band = zonal_band(r);
+    if (g.elem != 1 || band > 7) return DCT16A_EDOMAIN;
     if (band <= 3) return launch_ztpb<3>(src, g, r, recon, sse, st);
     if (band <= 5) return launch_ztpb<5>(src, g, r, recon, sse, st);
-    if (band <= 7) return launch_ztpb<7>(src, g, r, recon, sse, st);
-    return 1;
+    return launch_ztpb<7>(src, g, r, recon, sse, st);
 }
 
 }  // namespace dct16a
+#endif  // DCT16A_EXPERIMENTS

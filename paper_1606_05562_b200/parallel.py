@@ -6,11 +6,10 @@ exchange is the SUM all-reduce of the per-frame SSE vector: every rank writes
 its slice of an int64 [n_total] vector (zeros elsewhere) and one all-reduce
 yields both the per-frame and the global SSE (exact, order independent).
 torch.distributed provides the process group (NCCL on GPUs, gloo in the CPU
-tests); the per-frame work runs in libdct16a.
+tests and for several ranks sharing one GPU); every per-frame computation,
+the PSNR of each frame and of the whole set included, runs in libdct16a.
 """
 from __future__ import annotations
-
-import math
 
 
 def shard(n_items: int, world: int, rank: int) -> tuple[int, int]:
@@ -27,6 +26,8 @@ def reduce_sse(local_sse, offset: int, n_total: int, group=None):
     [n_total] vector and SUM all-reduce it across the group."""
     import torch
     import torch.distributed as dist
+    if offset < 0 or offset + local_sse.numel() > n_total:
+        raise ValueError(f"frames [{offset}, {offset + local_sse.numel()}) outside [0, {n_total})")
     full = torch.zeros(n_total, dtype=torch.int64, device=local_sse.device)
     full[offset:offset + local_sse.numel()] = local_sse
     if dist.is_available() and dist.is_initialized():
@@ -34,79 +35,80 @@ def reduce_sse(local_sse, offset: int, n_total: int, group=None):
     return full
 
 
-class FusedSseAllReduce:
-    """The config-4 exchange fused into the codec kernel (dct16a_codec_allreduce):
-    one int64 [n_total] SSE vector per rank in torch symmetric memory; every
-    rank's kernel adds each local frame's SSE into all ranks' vectors over
-    peer-mapped memory (NVLink).  Symmetric-memory barriers order the zeroing
-    before, and the reads after, every rank's kernel.  Reuse one instance."""
+def sse_psnr(full_sse, desc, stream=None):
+    """Per-frame PSNR, the exact ΣSSE and the PSNR of the whole set from an
+    all-reduced per-frame SSE vector, through the library's finaliser
+    (dct16a_sse_psnr, readings A7/A8).  Returns device
+    tensors (psnr float64 [n], sse_total int64 [1], psnr_total float64 [1])."""
+    import torch
+    from . import _lib
+    n = full_sse.numel()
+    psnr = torch.empty(n, dtype=torch.float64, device=full_sse.device)
+    tot = torch.empty(1, dtype=torch.int64, device=full_sse.device)
+    ptot = torch.empty(1, dtype=torch.float64, device=full_sse.device)
+    _lib.dct16a_sse_psnr(full_sse, n, desc, psnr, tot, ptot, stream)
+    return psnr, tot, ptot
 
-    def __init__(self, n_total: int, device, group=None):
+
+class FusedSseAllReduce:
+    """The config-4 exchange fused into the codec kernel (dct16a_codec_allreduce,
+    SURVEY.md §8(f) f2): one int64 [n_total] SSE vector per rank in torch
+    symmetric memory; every rank's kernel adds each local frame's SSE into all
+    ranks' vectors — through the NVLS multicast address when the group has one
+    (multimem.red: one store reaches every GPU through the NVSwitch), else by
+    peer-mapped atomics over NVLink.  Symmetric-memory barriers order the
+    zeroing before, and the reads after, every rank's kernel.  Reuse one
+    instance; the vector returned by run() is overwritten by the next run()."""
+
+    def __init__(self, n_total: int, device, group=None, use_multicast: bool = True):
         import torch
         import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm
-        self.n_total = n_total
-        self.buf = symm.empty(n_total, dtype=torch.int64, device=device)
+        self.n_total = int(n_total)
+        self.buf = symm.empty(self.n_total, dtype=torch.int64, device=device)
         self.handle = symm.rendezvous(self.buf, group if group is not None else dist.group.WORLD)
         self.peers = list(self.handle.buffer_ptrs)
         if len(self.peers) > 8:
             raise ValueError("dct16a_codec_allreduce supports up to 8 peers")
+        mc = int(getattr(self.handle, "multicast_ptr", 0) or 0) if use_multicast else 0
+        # the multicast address maps every rank's copy of the vector: one peer entry
+        self.targets = [mc] if mc else self.peers
+        self.multicast = bool(mc)
 
     def run(self, frames, quant, frame_offset: int, recon=None, desc=None, stream=None):
         """Codec of this rank's frames; returns the all-reduced per-frame SSE (int64)."""
+        import torch
         from . import _lib
+        n = 0 if frames is None else int(frames.shape[0])
+        if frame_offset < 0 or frame_offset + n > self.n_total:
+            raise ValueError(f"frames [{frame_offset}, {frame_offset + n}) outside the vector [0, {self.n_total})")
+        cur = torch.cuda.current_stream(self.buf.device)
+        if stream is not None and getattr(stream, "cuda_stream", stream) != cur.cuda_stream:
+            raise ValueError("run() must be called on torch's current stream (zeroing and barriers use it)")
         self.buf.zero_()
         self.handle.barrier()            # every rank's vector is zero before any kernel adds
-        if frames is not None and frames.shape[0] > 0:
-            _lib.dct16a_codec_allreduce(frames, quant, self.peers, frame_offset, recon, desc, stream)
+        if n > 0:
+            _lib.dct16a_codec_allreduce(frames, quant, self.targets, frame_offset, recon, desc, cur,
+                                        multicast=self.multicast)
         self.handle.barrier()            # every rank's kernel has finished adding
         return self.buf
-
-
-def psnr_from_sse(sse_total: int, n_pixels: int, bit_depth: int) -> float:
-    """10·log10(peak²·P/SSE), +inf for SSE = 0 (reading A7)."""
-    if sse_total == 0:
-        return math.inf
-    peak = (1 << bit_depth) - 1
-    return 10.0 * math.log10(peak * peak * n_pixels / sse_total)
 
 
 def codec_sharded(local_frames, offset: int, n_total: int, mode: str = "uniform", r: int = 16,
                   step: int = 16, valid_height: int | None = None, group=None, want_recon: bool = False):
     """Run the fused codec on this rank's frames and all-reduce the SSE.
-    Returns (recon or None, per-frame SSE int64 [n_total], global PSNR)."""
-    from . import codec
-    recon, sse_local, _ = codec(local_frames, mode, r=r, step=step, valid_height=valid_height,
-                                want_recon=want_recon)
-    full = reduce_sse(sse_local, offset, n_total, group)
-    n, h, w = local_frames.shape
-    vh = h if valid_height is None else valid_height
-    bits = 8 if local_frames.element_size() == 1 else 10
-    total = int(full.sum().item())
-    return recon, full, psnr_from_sse(total, n_total * vh * w, bits)
-
-
-def strided_ids(n_items: int, world: int, rank: int) -> list[int]:
-    """Items r, r + world, r + 2·world, ... — the ids rank `rank` generates when
-    every rank needs the whole batch (weak-scaling bench inputs)."""
-    if world < 1 or not 0 <= rank < world:
-        raise ValueError("bad world/rank")
-    return list(range(rank, n_items, world))
-
-
-def allgather_strided(part, n_items: int, world: int, group=None):
-    """Reassemble the full batch from every rank's strided part (part = items
-    rank, rank + world, ...; shape (len, ...)) with one all_gather of equal-size
-    padded buffers; returns the (n_items, ...) tensor in item order on every rank."""
+    Returns (recon or None, per-frame SSE int64 [n_total], per-frame PSNR
+    float64 [n_total], global PSNR float64 [1]) — device tensors."""
     import torch
-    import torch.distributed as dist
-    m = (n_items + world - 1) // world
-    buf = torch.zeros((m, *part.shape[1:]), dtype=part.dtype, device=part.device)
-    buf[:part.shape[0]] = part
-    parts = [torch.empty_like(buf) for _ in range(world)]
-    dist.all_gather(parts, buf, group=group)
-    out = torch.empty((n_items, *part.shape[1:]), dtype=part.dtype, device=part.device)
-    for r in range(world):
-        cnt = len(range(r, n_items, world))
-        out[r::world] = parts[r][:cnt]
-    return out
+    from . import _lib, codec
+    n, h, w = local_frames.shape
+    if n:
+        recon, sse_local, _ = codec(local_frames, mode, r=r, step=step, valid_height=valid_height,
+                                    want_recon=want_recon)
+    else:   # an empty shard still takes part in the collective
+        recon, sse_local = None, torch.empty(0, dtype=torch.int64, device=local_frames.device)
+    full = reduce_sse(sse_local, offset, n_total, group)
+    bits = _lib._pixel_depth(local_frames, None)
+    desc = _lib.make_desc(w, h, 1, bits, valid_height=valid_height)   # the geometry of one frame
+    psnr, _, ptot = sse_psnr(full, desc)
+    return recon, full, psnr, ptot

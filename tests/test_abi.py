@@ -23,7 +23,7 @@ def declared_symbols():
 def test_library_loads_and_exports_header_symbols():
     L = pkg.lib()
     syms = declared_symbols()
-    assert len(syms) == 13
+    assert len(syms) == 17
     for s in syms:
         assert hasattr(L, s), s
     out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
@@ -106,18 +106,92 @@ def test_binding_rejects_cpu_tensors():
 
 
 def test_options_validate_and_round_trip():
+    """The product library ships codec paths 0/2 and forward store modes
+    -1/3/5; the round-1 experiment variants (codec paths 1 and 3, store modes
+    0-2, 4, 6, 7) exist only in -DDCT16A_EXPERIMENTS builds."""
     old = pkg.dct16a_get_option(pkg.OPT_CODEC_PATH)
-    for v in (0, 1, 2, 3):
+    for v in (0, 2):
         pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, v)
         assert pkg.dct16a_get_option(pkg.OPT_CODEC_PATH) == v
     pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, old)
-    with pytest.raises(pkg.Dct16aError) as e:
-        pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, 4)
-    assert e.value.code == -5
+    for bad in (1, 3, 4, -1):
+        with pytest.raises(pkg.Dct16aError) as e:
+            pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, bad)
+        assert e.value.code == -5
+    old = pkg.dct16a_get_option(pkg.OPT_FWD_STORE)
+    for v in (-1, 3, 5):
+        pkg.dct16a_set_option(pkg.OPT_FWD_STORE, v)
+        assert pkg.dct16a_get_option(pkg.OPT_FWD_STORE) == v
+    pkg.dct16a_set_option(pkg.OPT_FWD_STORE, old)
+    for bad in (0, 1, 2, 4, 6, 7, 8):
+        with pytest.raises(pkg.Dct16aError):
+            pkg.dct16a_set_option(pkg.OPT_FWD_STORE, bad)
     with pytest.raises(pkg.Dct16aError) as e:
         pkg.dct16a_set_option(99, 0)
     assert e.value.code == -5
-    assert pkg.dct16a_get_option(pkg.OPT_FWD_STORE) in range(-1, 6)
+
+
+def test_library_is_the_trimmed_product_build():
+    """The experiment kernels are not in the shipped library."""
+    names = subprocess.run(["nm", "-C", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "fwd_kernel<1, 5>" in names and "codec_warp_kernel" in names and "zband_kernel" in names
+    assert "zonal_tpb_kernel" not in names and "codec_kernel(" not in names
+    assert "fwd_kernel<1, 0>" not in names and "fwd_kernel<1, 7>" not in names
+
+
+def test_overlapping_buffers_rejected():
+    """recon must not intersect src (not only recon == src), and coef must not
+    intersect src: the TMA stores would overwrite input tiles not yet read."""
+    L = pkg.lib()
+    d = pkg.make_desc(64, 64, 2, 8)                     # 2 images of 4 KB
+    q = pkg.make_quant("zonal", 16)
+    src, sse = 1 << 20, 1 << 24
+    for recon in (src + 16, src + 4096, src - 4096):
+        assert L.dct16a_codec(ctypes.c_void_p(src), ctypes.byref(d), ctypes.byref(q), ctypes.c_void_p(recon),
+                              ctypes.c_void_p(sse), None, None) == -5
+    assert "overlaps" in pkg.dct16a_last_error()
+    assert L.dct16a_forward(ctypes.c_void_p(src), ctypes.byref(d), ctypes.c_void_p(src + 8192 - 16), None) == -5
+    peers = (ctypes.c_void_p * 1)(ctypes.c_void_p(sse))
+    assert L.dct16a_codec_allreduce(ctypes.c_void_p(src), ctypes.byref(d), ctypes.byref(q), ctypes.c_void_p(src + 32),
+                                    peers, 1, 0, None) == -5
+
+
+def test_binding_checks_dtypes_and_sizes():
+    torch = pytest.importorskip("torch")
+    for bad in (torch.float32, torch.int32, torch.int64):
+        with pytest.raises(TypeError):
+            pkg.desc_of(torch.zeros((1, 16, 16), dtype=bad))
+    with pytest.raises(ValueError):
+        pkg.desc_of(torch.zeros((1, 16, 16), dtype=torch.uint8), bit_depth=10)
+    assert pkg.desc_of(torch.zeros((2, 32, 48), dtype=torch.int16)).bit_depth == 10
+    x = torch.zeros((1, 32, 32), dtype=torch.uint8)
+    with pytest.raises(ValueError, match="needs 1024"):
+        pkg.dct16a_forward(x, torch.zeros((3, 16, 16), dtype=torch.int32))
+    with pytest.raises(TypeError):
+        pkg.dct16a_forward(x, torch.zeros((4, 16, 16), dtype=torch.int64))
+    with pytest.raises(ValueError, match="needs 2"):
+        pkg.dct16a_codec(torch.zeros((2, 16, 16), dtype=torch.uint8), pkg.make_quant(), torch.zeros(1, dtype=torch.int64))
+    with pytest.raises(ValueError, match="descriptor spans"):
+        pkg.dct16a_forward(x, torch.zeros((4, 16, 16), dtype=torch.int32), pkg.make_desc(32, 32, 2, 8))
+
+
+def test_sse_psnr_and_forward_host_validation():
+    L = pkg.lib()
+    d = pkg.make_desc(64, 64, 1, 8)
+    buf = ctypes.c_void_p(1 << 20)
+    assert L.dct16a_sse_psnr(None, 4, ctypes.byref(d), None, None, None, None) == -1
+    assert L.dct16a_sse_psnr(buf, 0, ctypes.byref(d), None, None, None, None) == -2
+    assert L.dct16a_sse_psnr(ctypes.c_void_p((1 << 20) + 4), 4, ctypes.byref(d), None, None, None, None) == -4
+    d2 = pkg.make_desc(512, 512, 10, 8)
+    need1 = L.dct16a_forward_host_workspace(ctypes.byref(d2), 1)
+    assert need1 == 2 * (512 * 512 + 1024 * 1024)
+    assert L.dct16a_forward_host_workspace(ctypes.byref(d2), 4) == 4 * need1
+    assert L.dct16a_forward_host_workspace(ctypes.byref(d2), 0) == -5
+    h = ctypes.c_void_p(1 << 30)
+    assert L.dct16a_forward_host(None, ctypes.byref(d2), h, buf, need1, None) == -1
+    assert L.dct16a_forward_host(h, ctypes.byref(d2), h, ctypes.c_void_p((1 << 20) + 16), need1, None) == -4
+    assert L.dct16a_forward_host(h, ctypes.byref(d2), h, buf, need1 - 1, None) == -5
+    assert "workspace" in pkg.dct16a_last_error()
 
 
 def test_zonal_sweep_validation():
@@ -171,6 +245,10 @@ def test_codec_allreduce_validation():
     assert f(buf, ctypes.byref(d), ctypes.byref(q), None, None, 2, 0, None) == -1
     bad = (ctypes.c_void_p * 1)(ctypes.c_void_p((1 << 20) + 4))
     assert f(buf, ctypes.byref(d), ctypes.byref(q), None, bad, 1, 0, None) == -4
+    m = L.dct16a_codec_allreduce_multicast
+    assert m(buf, ctypes.byref(d), ctypes.byref(q), None, None, 0, None) == -1
+    assert m(buf, ctypes.byref(d), ctypes.byref(q), None, ctypes.c_void_p((2 << 20) + 4), 0, None) == -4
+    assert m(buf, ctypes.byref(d), ctypes.byref(q), None, ctypes.c_void_p(2 << 20), -1, None) == -5
 
 
 def test_build_flags_keep_subnormals():

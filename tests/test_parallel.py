@@ -1,6 +1,5 @@
 """Host logic of the multi-GPU path on CPU: contiguous sharding and the
 per-frame SSE all-reduce, with a real 2-process gloo group (127.0.0.1)."""
-import math
 import os
 import socket
 
@@ -25,9 +24,12 @@ def test_shard_covers_and_balances():
         parallel.shard(10, 2, 2)
 
 
-def test_psnr_from_sse():
-    assert parallel.psnr_from_sse(0, 10, 8) == math.inf
-    assert abs(parallel.psnr_from_sse(256, 256, 8) - 48.1308) < 1e-4
+def test_reduce_sse_rejects_out_of_range_shards():
+    with pytest.raises(ValueError):
+        parallel.reduce_sse(torch.zeros(3, dtype=torch.int64), 8, 10)
+    with pytest.raises(ValueError):
+        parallel.reduce_sse(torch.zeros(3, dtype=torch.int64), -1, 10)
+    assert parallel.reduce_sse(torch.arange(3, dtype=torch.int64), 7, 10).tolist() == [0] * 7 + [0, 1, 2]
 
 
 def _free_port():
@@ -64,32 +66,3 @@ def test_sse_allreduce_gloo(world, n_total):
     want = [(f * 7919) % 100003 + 2 ** 40 for f in range(n_total)]
     for r in range(world):
         assert out[r] == want          # every rank holds every frame's SSE, exactly
-
-
-def _gather_worker(rank, world, port, n_total, out):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    ids = parallel.strided_ids(n_total, world, rank)
-    part = torch.tensor([[i * 10 + j for j in range(3)] for i in ids], dtype=torch.int64).reshape(len(ids), 3)
-    full = parallel.allgather_strided(part, n_total, world)
-    out[rank] = full.tolist()
-    dist.destroy_process_group()
-
-
-@pytest.mark.parametrize("world,n_total", [(2, 7), (2, 8), (3, 10)])
-def test_allgather_strided_gloo(world, n_total):
-    """bench.py's input assembly: each rank generates items rank::world, one
-    all_gather rebuilds the batch in item order on every rank."""
-    ctx = mp.get_context("spawn")
-    mgr = ctx.Manager()
-    out = mgr.dict()
-    port = _free_port()
-    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, n_total, out)) for r in range(world)]
-    for p in procs:
-        p.start()
-    for p in procs:
-        p.join(120)
-        assert p.exitcode == 0
-    want = [[i * 10 + j for j in range(3)] for i in range(n_total)]
-    for r in range(world):
-        assert out[r] == want

@@ -7,7 +7,9 @@ vector over NCCL (paper_1606_05562_b200.parallel.reduce_sse).
 
 Launch: python -m torch.distributed.run --nnodes=1 --nproc-per-node N
         --master-addr 127.0.0.1 --master-port P tools/run_config4.py [--frames F]
-(or plainly with python for one GPU).  Rank 0 prints one JSON line: global
+(or plainly with python for one GPU).  With fewer GPUs than ranks (--backend
+gloo), ranks share the GPUs round-robin: the multi-rank logic (sharding, the
+all-reduce over CUDA tensors, the global PSNR) then runs on one B200.  Rank 0 prints one JSON line: global
 PSNR from ΣSSE, the per-frame SSE vector (--dump), codec time as the max over
 ranks (CUDA events), all-reduce time, blocks/s over all ranks.
 """
@@ -35,6 +37,7 @@ def main():
     ap.add_argument("--step", type=int, default=16)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--dump", action="store_true", help="print the per-frame SSE vector")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--fused", action="store_true",
                     help="fuse the SSE all-reduce into the kernel (dct16a_codec_allreduce over symmetric memory) "
                          "and check it against the NCCL path")
@@ -43,12 +46,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % torch.cuda.device_count()     # ranks share GPUs when there are fewer GPUs than ranks
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1 or a.fused:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29561")
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+        if a.backend == "nccl":
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+        else:
+            dist.init_process_group("gloo", rank=rank, world_size=world)
 
     f0, f1 = parallel.shard(a.frames, world, rank)
     x = torch.from_numpy(synth.frames_10bit(range(f0, f1), H=a.height, W=a.width, total=1000)).to(dev)
@@ -83,31 +90,43 @@ def main():
     ar_ms = torch.tensor([r0.elapsed_time(r1)], dtype=torch.float64, device=dev)
     fused = None
     if a.fused:
-        fz = parallel.FusedSseAllReduce(a.frames, dev)
-        got = fz.run(x if n else None, q, f0, None, d, stream)
-        torch.cuda.synchronize()
-        f_e0, f_e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f_e0.record(stream)
-        for _ in range(a.reps):
+        try:
+            fz = parallel.FusedSseAllReduce(a.frames, dev)
+        except Exception as e:   # e.g. symmetric memory with several ranks on one GPU
+            fused = {"skipped": f"{type(e).__name__}: {str(e).splitlines()[0][:200] if str(e) else ''}"}
+        else:
             got = fz.run(x if n else None, q, f0, None, d, stream)
-        f_e1.record(stream)
-        f_e1.synchronize()
-        fused = {"ms": f_e0.elapsed_time(f_e1) / a.reps, "equal_to_nccl": bool(torch.equal(got, full))}
+            torch.cuda.synchronize()
+            f_e0, f_e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f_e0.record(stream)
+            for _ in range(a.reps):
+                got = fz.run(x if n else None, q, f0, None, d, stream)
+            f_e1.record(stream)
+            f_e1.synchronize()
+            fused = {"ms": f_e0.elapsed_time(f_e1) / a.reps, "equal_to_nccl": bool(torch.equal(got, full)),
+                     "n_peers": len(fz.targets), "multicast": fz.multicast}
     if world > 1:
+        if a.backend == "gloo":
+            ms, ar_ms = ms.cpu(), ar_ms.cpu()
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         dist.all_reduce(ar_ms, op=dist.ReduceOp.MAX)
+    psnr_frames, sse_tot, psnr_tot = parallel.sse_psnr(full, pkg.make_desc(a.width, a.height, 1, 10))
+    torch.cuda.synchronize()
     if rank == 0:
-        tot = int(full.sum().item())
+        tot = int(sse_tot.item())
+        assert tot == int(full.sum().item())
         P = a.frames * a.height * a.width
         blocks = a.frames * (a.height // 16) * (a.width // 16)
         line = {"config": 4, "n_gpus": world, "frames": a.frames, "step": a.step,
                 "codec_ms_max_over_ranks": float(ms.item()), "allreduce_ms": float(ar_ms.item()),
                 "blocks_per_s": blocks / (float(ms.item()) / 1e3),
-                "global_psnr_db": parallel.psnr_from_sse(tot, P, 10), "sse_total": tot}
+                "global_psnr_db": float(psnr_tot.item()), "sse_total": tot, "backend": a.backend if world > 1 else None,
+                "pixels": P}
         if fused is not None:
             line["fused_allreduce"] = fused
         if a.dump:
             line["sse"] = full.cpu().tolist()
+            line["psnr"] = psnr_frames.cpu().tolist()
         print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.destroy_process_group()
