@@ -459,7 +459,7 @@ def run_ours(args):
         if world == 1 and not args.no_cpu_baseline:
             workers = host_cores()
             cpu = cpu_model()
-            n_s = int(os.environ.get("DCT16A_ORACLE_IMAGES", "1024"))
+            n_s = int(os.environ.get("DCT16A_ORACLE_IMAGES", "4096"))
             imgs = synth.batch_u8(range(n_s), H, W)
             r, cs, wall = oracle_rate("cfg2", imgs, workers)
             line["cpu_baseline"] = {"value": r, "unit": "blocks/s", "cores": workers, "cpu": cpu, "kind": "oracle",
