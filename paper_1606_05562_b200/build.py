@@ -11,7 +11,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libdct16a.so")
 BUILD = os.path.join(ROOT, "build", "obj")   # object files (git-ignored), never in csrc/
-SOURCES = ["abi.cu", "forward.cu", "codec.cu", "zonal_tpb.cu", "zonal_band.cu", "codec_warp.cu", "sweep.cu", "ssim.cu"]
+SOURCES = ["abi.cu", "forward.cu", "codec.cu", "zonal_tpb.cu", "zonal_band.cu", "codec_warp.cu", "codec_uniform.cu", "sweep.cu", "ssim.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v", "--expt-relaxed-constexpr",

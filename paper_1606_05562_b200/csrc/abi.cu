@@ -150,7 +150,7 @@ int env_int(const char* name, int dflt) {
 // (the defaults); -DDCT16A_EXPERIMENTS adds the round-1 variants.
 bool codec_path_built(int v) {
 #ifdef DCT16A_EXPERIMENTS
-    return v >= 0 && v <= 3;
+    return v >= 0 && v <= 4;
 #else
     return v == 0 || v == 2;
 #endif

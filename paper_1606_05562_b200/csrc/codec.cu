@@ -510,8 +510,9 @@ int launch_codec_generic(const void* src, const Geom& g, const dct16a_quant& q, 
 //           everything else -> warp-per-block-pair kernel (codec_warp.cu);
 //   2: always codec_warp.cu.
 // Experiment builds (-DDCT16A_EXPERIMENTS) add 1 (zonal on the generic kernel
-// above) and 3 (zonal 8-bit r <= 36 on the thread-per-block kernel,
-// zonal_tpb.cu).  Every path computes the same bytes.
+// above), 3 (zonal 8-bit r <= 36 on the thread-per-block kernel, zonal_tpb.cu)
+// and 4 (uniform on the two-blocks-per-lane kernel, codec_uniform.cu).  Every
+// path computes the same bytes.
 int launch_codec(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse,
                  double* psnr, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(uint64_t) * g.N, st);
@@ -523,6 +524,9 @@ int launch_codec(const void* src, const Geom& g, const dct16a_quant& q, void* re
 #ifdef DCT16A_EXPERIMENTS
     else if (zonal && path == 3 && zonal_band_applies(g, q.r)) rc = launch_zonal_tpb(src, g, q.r, recon, sse, st);
     else if (zonal && path == 1) rc = launch_codec_generic(src, g, q, recon, sse, st);
+#endif
+#ifdef DCT16A_EXPERIMENTS
+    else if (!zonal && path == 4) rc = launch_codec_uniform(src, g, q, recon, sse, st, nullptr, 0, 0, 0);
 #endif
     else rc = launch_codec_warp(src, g, q, recon, sse, st);
     if (rc) return rc;

@@ -53,6 +53,7 @@
 #include "tables.cuh"
 #include "tile128.cuh"
 #include "uexact.cuh"
+#include "uexact_tile.cuh"
 
 namespace dct16a {
 namespace {
@@ -114,54 +115,6 @@ struct WParams {
     float magic_f, half_delta;
     uint32_t magic_bits;
 };
-
-// Exact levels of one block recomputed from its pixels (rare branch): Z by the
-// integer network, then the exact uniform decision (uniform_level/uniform_fix).
-template <int ELEM>
-__device__ __noinline__ void exact_levels_from_stage(const uint8_t* stage, int bb, int step, int32_t* q) {
-    int32_t Y[16][16];
-    for (int t = 0; t < 16; ++t) {
-        int a0, a1;
-        row_addr<ELEM>(bb, t, &a0, &a1);
-        uint32_t w[4 * ELEM];
-        load_px<ELEM>(stage, a0, a1, w);
-        int32_t x[16], y[16];
-        for (int j = 0; j < 16; ++j) x[j] = px_of<ELEM>(w, j);
-        net_fwd(x, y);
-        for (int l = 0; l < 16; ++l) Y[t][l] = y[l];
-    }
-    for (int l = 0; l < 16; ++l) {
-        int32_t c[16], z[16];
-        for (int t = 0; t < 16; ++t) c[t] = Y[t][l];
-        net_fwd(c, z);
-        for (int k = 0; k < 16; ++k) {
-            const uint32_t az = static_cast<uint32_t>(z[k] < 0 ? -z[k] : z[k]);
-            const uint64_t d2g = static_cast<uint64_t>(step) * step * (g_of(k) * g_of(l));
-            const double e = static_cast<double>(az) / (step * sqrt(static_cast<double>(g_of(k) * g_of(l)))) + 0.5;
-            const int32_t m = uniform_fix(az, static_cast<int32_t>(floor(e)), d2g);
-            q[k * 16 + l] = z[k] < 0 ? -m : m;
-        }
-    }
-}
-
-// Rare branch of the uniform rounding: row t of the block has a pixel within
-// 2^-20 of a .5 boundary.  Recompute the row from the transposition tile (still
-// intact), flag the near pixels again and decide them exactly from the levels.
-template <int ELEM>
-__device__ __noinline__ void exact_row_fix(const uint8_t* stage, int bb, const double* urow, int t, int step,
-                                           int maxpix, int* pix) {
-    double rr[16], a[16];
-    for (int j = 0; j < 16; ++j) rr[j] = urow[j];
-    net_inv(rr, a);
-    int32_t qb[256];
-    exact_levels_from_stage<ELEM>(stage, bb, step, qb);
-    for (int j = 0; j < 16; ++j) {
-        bool nr;
-        int n0;
-        round_f64(a[j], nr, n0);
-        if (nr) pix[j] = min(max(uniform_exact_floor(qb, t, j, step, n0), 0), maxpix);
-    }
-}
 
 // Exact uniform level for a coefficient whose float estimate m is flagged (rare).
 __device__ __noinline__ int32_t uniform_fix_call(float z, int32_t m, int step, int G) {
@@ -302,7 +255,7 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
                 load_px<ELEM>(stage, a0, a1, w);
                 float x[16], y[16];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) x[j] = static_cast<float>(px_of<ELEM>(w, j));
+                for (int j = 0; j < 16; ++j) x[j] = px_float<ELEM>(w, j);
                 net_fwd(x, y);
 #pragma unroll
                 for (int q = 0; q < 4; ++q)

@@ -55,6 +55,11 @@ int launch_zonal_tpb(const void* src, const Geom& g, int r, void* recon, uint64_
 // warp-per-block-pair codec (uniform, and zonal cases zonal_tpb does not take)
 int launch_codec_warp(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse,
                       cudaStream_t st);
+#ifdef DCT16A_EXPERIMENTS
+// uniform-quantiser codec, two blocks per lane (codec_uniform.cu); n_peers = 0: local sse
+int launch_codec_uniform(const void* src, const Geom& g, const dct16a_quant& q, void* recon, uint64_t* sse,
+                         cudaStream_t st, uint64_t* const* peers, int n_peers, long long frame_offset, int multicast);
+#endif
 // mean SSIM per image (ssim.cu)
 int launch_ssim(const void* ref, const void* test, const Geom& g, double* ssim, cudaStream_t st);
 // zonal r-sweep (sweep.cu) and the shared PSNR finaliser
@@ -79,7 +84,7 @@ int get_option(int option);
 // family's slot table locked in between.  A launch being captured into a CUDA
 // graph gets slot -1: the static schedule, so overlapping replays of one graph
 // are safe.
-enum SchedFamily { kSchedForward = 0, kSchedBand = 1, kSchedCodecWarp = 2, kSchedFamilies = 3 };
+enum SchedFamily { kSchedForward = 0, kSchedBand = 1, kSchedCodecWarp = 2, kSchedCodecUniform = 3, kSchedFamilies = 4 };
 class SchedGuard {
   public:
     SchedGuard(int family, cudaStream_t st);

@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
                 float x[16], y[16];
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
-                    x[j] = static_cast<float>(px_of<ELEM>(w, j));
+                    x[j] = px_float<ELEM>(w, j);
                     xs[j] = 8388608.0f + x[j];
                 }
                 net_fwd(x, y);

@@ -131,4 +131,12 @@ __device__ __forceinline__ int px_of(const uint32_t (&w)[4 * ELEM], int j) {
                      : static_cast<int>((w[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
 }
 
+// pixel j of a packed row as float (unsigned extraction: one I2F.U8/U16 with a
+// byte / half selector)
+template <int ELEM>
+__device__ __forceinline__ float px_float(const uint32_t (&w)[4 * ELEM], int j) {
+    return ELEM == 1 ? static_cast<float>((w[j >> 2] >> (8 * (j & 3))) & 0xFFu)
+                     : static_cast<float>((w[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+}
+
 }  // namespace dct16a

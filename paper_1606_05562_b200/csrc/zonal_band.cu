@@ -45,6 +45,7 @@
 
 #include "internal.h"
 #include "net16.cuh"
+#include "pack2.cuh"
 #include "ptx.cuh"
 #include "sched.cuh"
 #include "quant.cuh"
@@ -76,15 +77,6 @@ static_assert(4 * kTyBlock * 4 <= kBXpose, "transposition buffer too small");
 constexpr int kBWarpBytes = kBStages * kBStage;
 // + per warp: kBStages mbarriers and the coordinates (n, by, tb, valid) of the tile in each stage
 constexpr int kBSmem = 1024 + kBWarps * (kBWarpBytes + kBXpose) + kBWarps * kBStages * (8 + 16);
-
-// two float32 lanes processed by one FADD2/FFMA2 (sm_100): the two blocks of a pair
-struct F2 {
-    float2 v;
-};
-__device__ __forceinline__ F2 operator+(F2 a, F2 b) { return F2{__fadd2_rn(a.v, b.v)}; }
-__device__ __forceinline__ F2 operator-(F2 a, F2 b) { return F2{__fadd2_rn(a.v, make_float2(-b.v.x, -b.v.y))}; }
-__device__ __forceinline__ F2 operator-(F2 a) { return F2{make_float2(-a.v.x, -a.v.y)}; }
-__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) { return F2{__ffma2_rn(a.v, b.v, c.v)}; }
 
 #ifndef DCT16A_ZB_PROMO
 #define DCT16A_ZB_PROMO 0   // input L2 promotion: none (256 B promotion re-reads ~20 % of the input)
