@@ -972,3 +972,38 @@ def test_fused_allreduce_multi_gpu_equals_nccl():
     assert line["fused_allreduce"]["equal_to_nccl"] is True
     ref = oc.codec_images(synth.frames_10bit(range(11), H=64, W=208, workers=1), "uniform", step=16, bit_depth=10)
     assert line["sse"] == ref["sse"]
+
+
+@pytest.mark.parametrize("bd", [8, 10])
+def test_band_kernel_every_r_up_to_136(bd):
+    """The band-pruned zonal kernel (codec path 0) for every r it serves,
+    1..136 (bands 3/5/7/11/15; one or two columns per lane), 8- and 10-bit,
+    on a ragged strip (17 blocks: a partial tile) with pitched rows: pixels
+    and SSE equal the oracle, and the warp kernel (path 2) byte for byte."""
+    hi = 256 if bd == 8 else 1024
+    rng = np.random.default_rng(77 + bd)
+    if bd == 8:
+        base = synth.batch_u8([20, 21], 48, 288)
+    else:
+        base = synth.frames_10bit([5, 6], H=48, W=288, workers=1)
+    base[0, :4, :16] = hi - 1                         # saturated corner: clamping at the top
+    base[1, 8:16, 32:64] = 0                          # and at the bottom
+    view = base[:, :, :272]
+    vc = np.ascontiguousarray(view)
+    t = to_dev(base)[:, :, :272]
+    old = pkg.dct16a_get_option(pkg.OPT_CODEC_PATH)
+    try:
+        for r in range(1, 137):
+            pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, 0)
+            rec, sse, _ = pkg.codec(t, "zonal", r=r)
+            pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, 2)
+            rec2, sse2, _ = pkg.codec(t, "zonal", r=r)
+            torch.cuda.synchronize()
+            assert torch.equal(rec, rec2) and torch.equal(sse, sse2), r
+            if r in (1, 2, 6, 7, 10, 15, 16, 21, 28, 29, 36, 37, 45, 64, 66, 78, 79, 100, 120, 136):
+                ref = oc.codec_images(vc, "zonal", r=r, bit_depth=bd)
+                assert np.array_equal(rec.cpu().numpy(), ref["recon_img"]), r
+                assert sse.cpu().tolist() == ref["sse"], r
+    finally:
+        pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, old)
+    del rng

@@ -36,15 +36,20 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--frames", type=int, default=600)
     ap.add_argument("--reps", type=int, default=20)
-    ap.add_argument("--paths", default="0,3,2")
-    ap.add_argument("--r", default="16,32")
+    ap.add_argument("--paths", default="0,2")
+    ap.add_argument("--r", default="16,32,64,128")
+    ap.add_argument("--bits", type=int, default=8, help="10: config-3 geometry with 10-bit frames (config-4 recipe)")
     args = ap.parse_args()
     peak = 6548.2
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         peak = json.load(open(p)).get("hbm_gbs", peak)
-    cases = [("config 1", torch.from_numpy(synth.image_u8(0)[None]).cuda(), None),
-             ("config 3", torch.from_numpy(synth.video_u8(args.frames)).cuda(), 1080)]
+    if args.bits == 8:
+        cases = [("config 1", torch.from_numpy(synth.image_u8(0)[None]).cuda(), None),
+                 ("config 3", torch.from_numpy(synth.video_u8(args.frames)).cuda(), 1080)]
+    else:
+        f = torch.from_numpy(synth.frames_10bit(range(16), H=1088, W=1920)).cuda()
+        cases = [("10-bit 1088x1920", f[torch.arange(args.frames, device="cuda") % 16], None)]
     old = pkg.dct16a_get_option(pkg.OPT_CODEC_PATH)
     for name, x, vh in cases:
         n, h, w = x.shape
