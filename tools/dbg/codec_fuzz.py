@@ -1,4 +1,4 @@
-"""One-off fuzz of the fused codec on every kernel path: random geometries
+"""Fuzz of the fused codec on every kernel path: random geometries
 (ragged widths, pitched/strided windows, valid_height < H, batches 1-3),
 8/10-bit, zonal (random r) and uniform (random step), smooth and noise content,
 against the oracle byte for byte."""
@@ -12,6 +12,8 @@ import paper_1606_05562_b200 as pkg  # noqa: E402
 from oracle import codec as oc  # noqa: E402
 
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 100
+# the product library's kernel choices; an experiment build (DCT16A_LIB) adds 1, 3, 4
+PATHS = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 2]
 rng = np.random.default_rng(777)
 bad = 0
 for c in range(cases):
@@ -29,11 +31,12 @@ for c in range(cases):
     view = np.ascontiguousarray(base[:, :H, :W])
     t = torch.from_numpy(base).cuda()[:, :H, :W]
     mode = "zonal" if rng.random() < 0.5 else "uniform"
-    r = int(rng.integers(1, 257)) if rng.random() < 0.5 else int(rng.integers(1, 37))
+    u = rng.random()
+    r = int(rng.integers(1, 257)) if u < 0.3 else (int(rng.integers(1, 37)) if u < 0.6 else int(rng.integers(37, 137)))
     step = int(rng.integers(1, 120))
     vh = int(rng.integers(1, H + 1)) if rng.random() < 0.3 else None
     ref = oc.codec_images(view, mode, r=r, step=step, bit_depth=bd, valid_height=vh)
-    for path in (0, 1, 2, 3):
+    for path in PATHS:
         pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, path)
         rec, sse, _ = pkg.codec(t, mode, r=r, step=step, valid_height=vh)
         torch.cuda.synchronize()
@@ -42,4 +45,4 @@ for c in range(cases):
             bad += 1
             print("MISMATCH", c, path, bd, mode, n, H, W, r, step, vh)
 pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, 0)
-print(f"codec fuzz: {cases} cases x 4 paths, {bad} mismatches")
+print(f"codec fuzz: {cases} cases x {len(PATHS)} paths {PATHS}, {bad} mismatches")
