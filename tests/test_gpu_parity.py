@@ -1007,3 +1007,27 @@ def test_band_kernel_every_r_up_to_136(bd):
     finally:
         pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, old)
     del rng
+
+
+def test_fused_allreduce_several_peer_vectors_one_gpu():
+    """The n_peers > 1 branch of dct16a_codec_allreduce on one GPU: three
+    'ranks' (three frame shards, launched concurrently on three streams) each
+    add every frame's SSE into all three per-rank vectors (here plain device
+    buffers of one process instead of peer-mapped symmetric memory); every
+    vector ends with every frame's SSE, equal to the oracle, and to the NCCL
+    form's reduce-by-offset."""
+    f = synth.frames_10bit(range(9), H=64, W=208, workers=1)
+    x = to_dev(f)
+    q = pkg.make_quant("uniform", 16, 16)
+    vecs = [torch.zeros(9, dtype=torch.int64, device=DEV) for _ in range(3)]
+    peers = [v.data_ptr() for v in vecs]
+    streams = [torch.cuda.Stream(DEV) for _ in range(3)]
+    torch.cuda.synchronize()
+    for rank, (a, b) in enumerate([(0, 3), (3, 5), (5, 9)]):
+        shard = x[a:b]
+        with torch.cuda.stream(streams[rank]):
+            pkg.dct16a_codec_allreduce(shard, q, peers, a, None, pkg.desc_of(shard), streams[rank])
+    torch.cuda.synchronize()
+    ref = oc.codec_images(f, "uniform", step=16, bit_depth=10)
+    for v in vecs:
+        assert v.cpu().tolist() == ref["sse"]
