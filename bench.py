@@ -288,8 +288,11 @@ def leg_cfg4(c: Ctx, args, peak):
     if ids:
         part[:len(ids)] = torch.from_numpy(synth.frames_10bit(ids, workers=max(1, host_cores() // c.world))).to(c.dev)
     if c.world > 1:
-        parts = [torch.empty_like(part) for _ in range(c.world)]
-        c.dist.all_gather(parts, part)
+        # as bytes: NCCL (and gloo) have no int16 type
+        pb = part.view(torch.uint8)
+        parts_b = [torch.empty_like(pb) for _ in range(c.world)]
+        c.dist.all_gather(parts_b, pb)
+        parts = [t.view(torch.int16) for t in parts_b]
     else:
         parts = [part]
     distinct = torch.empty((K, 2160, 3840), dtype=torch.int16, device=c.dev)
@@ -340,7 +343,7 @@ def leg_cfg4(c: Ctx, args, peak):
            "blocks_per_s": blocks / ms * 1e3, "alg_bytes_per_block": 1024, "alg_GBs": alg / ms / 1e6,
            "bound": "hbm", "frac": alg / ms / 1e6 / peak, "global_psnr_db": float(ptot.item()),
            "sse_total": int(tot.item()), "sse_matches_fixtures": ok,
-           "collective": "nccl all_reduce" if c.world > 1 else "none (1 rank)"}
+           "collective": f"{c.dist.get_backend()} all_reduce" if c.world > 1 else "none (1 rank)"}
     sample = distinct[:6].cpu().numpy() if c.rank == 0 and c.world == 1 else None
     return out, sample
 
@@ -382,11 +385,17 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # NCCL between GPUs; DCT16A_BENCH_BACKEND=gloo exercises the N > 1 path
+        # with several ranks on one GPU (functional check only, not a measurement)
+        backend = os.environ.get("DCT16A_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     c = Ctx(torch, dist, world, rank, dev)
     peak, peak_src = peaks()
 
