@@ -336,16 +336,36 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
                     }
                     if (!valid) nmin = 0xFFFFFFFFu;
                     if (__any_sync(0xffffffffu, nmin < 8192u)) {
+                        // the row's float64 values, from the transposition tile before the
+                        // level computation below reuses it (local memory: rare branch only)
+                        double arow[16];
                         if (nmin < 8192u) {
-                            int fix[16];   // local memory, rare branch only
+                            double rin[16];
+                            for (int j = 0; j < 16; ++j) rin[j] = tu[t * 17 + j];
+                            net_inv(rin, arow);
+                        }
+                        __syncwarp();
+                        // the exact levels of both blocks of the pair, computed once by their
+                        // lanes from the ORIGINAL pixels (no lane has written its
+                        // reconstruction yet), then — when a block with levels in
+                        // irrational cells has a pixel to decide — the four integer
+                        // components of every row (scratch: this half's 2.5 KB of the tile)
+                        int32_t* qs = reinterpret_cast<int32_t*>(xpose) + h * 640;
+                        const bool irr = block_levels_coop<ELEM>(stage, bb, t, p.step, qs);
+                        const bool rational = ((__ballot_sync(0xffffffffu, irr) >> (16 * h)) & 0xFFFFu) == 0;
+                        int32_t J[4][16];
+                        if (__any_sync(0xffffffffu, nmin < 8192u && !rational))
+                            block_components_coop(qs, qs + 320, t, J);
+                        if (nmin < 8192u) {
+                            int fix[16];
 #pragma unroll
                             for (int j = 0; j < 16; ++j) fix[j] = pix[j];
-                            exact_row_fix<ELEM>(stage, bb, tu + t * 17, t, p.step, p.maxpix, fix);
+                            exact_row_fix_levels(arow, J, rational, p.step, p.maxpix, fix);
 #pragma unroll
                             for (int j = 0; j < 16; ++j) pix[j] = fix[j];
                         }
-                        // the exact fix re-reads the whole block's ORIGINAL pixels from the
-                        // stage: no lane may overwrite its row with the reconstruction before
+                        // the tile is rewritten next, and the levels were read from the
+                        // ORIGINAL pixels: no lane may write its reconstruction before
                         __syncwarp();
                     }
                 } else {

@@ -11,9 +11,10 @@
 
 namespace dct16a {
 
-// Forward network, stage by stage as printed in Eq. (1).
+// Forward network, stage by stage as printed in Eq. (1).  Also usable in
+// constant expressions (uexact.cuh builds T from it at compile time).
 template <typename V>
-__device__ __forceinline__ void net_fwd(const V (&x)[16], V (&y)[16]) {
+__host__ __device__ __forceinline__ constexpr void net_fwd(const V (&x)[16], V (&y)[16]) {
     // M1 = [[I8, Ī8], [Ī8, -I8]]: 16 additions
     const V a0 = x[0] + x[15], a1 = x[1] + x[14], a2 = x[2] + x[13], a3 = x[3] + x[12];
     const V a4 = x[4] + x[11], a5 = x[5] + x[10], a6 = x[6] + x[9], a7 = x[7] + x[8];

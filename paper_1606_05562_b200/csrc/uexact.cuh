@@ -46,23 +46,27 @@ __device__ __forceinline__ int sign_q23(long long b0, long long b1, long long b2
     return sign_r2(R, S) > 0 ? sp : sq;
 }
 
-// T as a table, column i of T = net_fwd(e_i) (the network of Eq. (1)).
-__device__ __forceinline__ void t_table(int8_t (&T)[16][16]) {
+// T as a table, built at compile time: column i of T = net_fwd(e_i) (the
+// network of Eq. (1)).
+struct TTable {
+    int8_t v[16][16];
+};
+constexpr TTable make_t_table() {
+    TTable t{};
     for (int i = 0; i < 16; ++i) {
-        int32_t x[16], y[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) x[j] = j == i;
+        int32_t x[16] = {}, y[16] = {};
+        x[i] = 1;
         net_fwd(x, y);
-#pragma unroll
-        for (int k = 0; k < 16; ++k) T[k][i] = static_cast<int8_t>(y[k]);
+        for (int k = 0; k < 16; ++k) t.v[k][i] = static_cast<int8_t>(y[k]);
     }
+    return t;
 }
+static __constant__ TTable c_T = make_t_table();
 
-// floor(A′[i][j] + 1/2) exactly, for the levels q (row-major k, l) and step Δ,
-// given N0 = the integer nearest to the float64 value of A′ + 1/2.
-static __device__ __noinline__ int uniform_exact_floor(const int32_t* q, int i, int j, int step, int N0) {
-    int8_t T[16][16];
-    t_table(T);
+// floor(A′[i][j] + 1/2) exactly, for the levels q (q[k·qs + l], row stride qs)
+// and step Δ, given N0 = the integer nearest to the float64 value of A′ + 1/2.
+static __device__ __noinline__ int uniform_exact_floor(const int32_t* q, int i, int j, int step, int N0, int qs = 16) {
+    const auto& T = c_T.v;
     const int e[3] = {3, 2, 3};
     const int r2[3] = {1, 3, 2};
     long long J1 = 0, J2 = 0, J3 = 0, J6 = 0;
@@ -70,7 +74,7 @@ static __device__ __noinline__ int uniform_exact_floor(const int32_t* q, int i, 
         if (T[k][i] == 0) continue;
         const int ck = uclass(k);
         for (int l = 0; l < 16; ++l) {
-            const int v = q[k * 16 + l];
+            const int v = q[k * qs + l];
             if (v == 0 || T[l][j] == 0) continue;
             const int cl = uclass(l);
             const long long t = static_cast<long long>(T[k][i] * T[l][j]) * v * (e[ck] * e[cl]);
@@ -82,6 +86,16 @@ static __device__ __noinline__ int uniform_exact_floor(const int32_t* q, int i, 
     }
     const long long b0 = step * J1 + 72 - 144LL * N0;
     return sign_q23(b0, step * J2, step * J3, step * J6) >= 0 ? N0 : N0 - 1;
+}
+
+// floor(A′ + 1/2) exactly when every nonzero level of the block lies in a
+// rational cell (g_k = g_l): then A′ = Δ·J1/144 with J1 an integer (the √2, √3,
+// √6 components vanish), recovered from the float64 value a of A′ (|error| far
+// below 1/2 unit of J1), and floor((Δ·J1 + 72)/144) is integer arithmetic.
+__device__ __forceinline__ int uniform_rational_floor(double a, int step) {
+    const long long J1 = __double2ll_rn(a * 144.0 / step);
+    const long long num = static_cast<long long>(step) * J1 + 72;
+    return static_cast<int>(num >= 0 ? num / 144 : -((-num + 143) / 144));
 }
 
 // Rounding of a float64 reconstruction value a = A′ (reading A6): floor(a + 1/2)
