@@ -31,12 +31,18 @@ namespace dct16a {
 // of 64 int4 (one 16x16 block), so every thread always sees the same four
 // cells (k, l0..l0+3): their zig-zag mask, scale s_k·s_l and exact-decision
 // constants are computed once per thread.  Streaming loads/stores (.cs).
+constexpr int kQUnroll = 4;   // int4 groups in flight per thread
+
 __global__ void __launch_bounds__(256) quantize_kernel(const int4* __restrict__ coef, int4* __restrict__ qcoef,
-                                                       float4* __restrict__ scaled, long long n4, int mode, int r,
-                                                       int step) {
-    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;   // multiple of 64
-    long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    const int pos = static_cast<int>((i * 4) & 255);
+                                                       float4* __restrict__ scaled, long long n4, long long chunk,
+                                                       int mode, int r, int step) {
+    // CTA b owns the contiguous int4 range [b·chunk, (b+1)·chunk) (chunk a multiple
+    // of 256·kQUnroll), walked kQUnroll·256 int4 at a time with every load of a
+    // round issued before any store: a compact address window per CTA, several
+    // 16-byte loads in flight per thread
+    const long long base = blockIdx.x * chunk;
+    const long long lim = min(base + chunk, n4);
+    const int pos = static_cast<int>((threadIdx.x * 4) & 255);   // the same 4 cells on every visit
     const int k = pos >> 4, l0 = pos & 15;
     float sc[4], cq[4];
     uint64_t d2g[4];
@@ -50,23 +56,31 @@ __global__ void __launch_bounds__(256) quantize_kernel(const int4* __restrict__ 
         d2g[e] = static_cast<uint64_t>(step) * step * (g_of(k) * g_of(l));
         keep[e] = zigzag_rank(k, l) < r;
     }
-    if (mode == DCT16A_ZONAL) {
-        for (; i < n4; i += stride) {
-            const int4 z = __ldcs(coef + i);
-            const int q0 = keep[0] ? z.x : 0, q1 = keep[1] ? z.y : 0, q2 = keep[2] ? z.z : 0, q3 = keep[3] ? z.w : 0;
-            __stcs(qcoef + i, make_int4(q0, q1, q2, q3));
-            if (scaled)
-                __stcs(scaled + i, make_float4(sc[0] * static_cast<float>(q0), sc[1] * static_cast<float>(q1),
-                                               sc[2] * static_cast<float>(q2), sc[3] * static_cast<float>(q3)));
+    for (long long i0 = base + threadIdx.x; i0 < lim; i0 += 256 * kQUnroll) {
+        int4 z[kQUnroll];
+#pragma unroll
+        for (int u = 0; u < kQUnroll; ++u) {
+            const long long i = i0 + 256LL * u;
+            z[u] = i < lim ? __ldcs(coef + i) : make_int4(0, 0, 0, 0);
         }
-    } else {
-        for (; i < n4; i += stride) {
-            const int4 z = __ldcs(coef + i);
-            __stcs(qcoef + i, make_int4(uniform_level(z.x, cq[0], d2g[0]), uniform_level(z.y, cq[1], d2g[1]),
-                                        uniform_level(z.z, cq[2], d2g[2]), uniform_level(z.w, cq[3], d2g[3])));
-            if (scaled)
-                __stcs(scaled + i, make_float4(sc[0] * static_cast<float>(z.x), sc[1] * static_cast<float>(z.y),
-                                               sc[2] * static_cast<float>(z.z), sc[3] * static_cast<float>(z.w)));
+#pragma unroll
+        for (int u = 0; u < kQUnroll; ++u) {
+            const long long i = i0 + 256LL * u;
+            if (i >= lim) break;
+            int4 q;
+            if (mode == DCT16A_ZONAL) {
+                q = make_int4(keep[0] ? z[u].x : 0, keep[1] ? z[u].y : 0, keep[2] ? z[u].z : 0, keep[3] ? z[u].w : 0);
+            } else {
+                q = make_int4(uniform_level(z[u].x, cq[0], d2g[0]), uniform_level(z[u].y, cq[1], d2g[1]),
+                              uniform_level(z[u].z, cq[2], d2g[2]), uniform_level(z[u].w, cq[3], d2g[3]));
+            }
+            __stcs(qcoef + i, q);
+            if (scaled) {
+                // zonal: s_k·s_l·(Z ⊙ M_r); uniform: s_k·s_l·Z
+                const int4 v = mode == DCT16A_ZONAL ? q : z[u];
+                __stcs(scaled + i, make_float4(sc[0] * static_cast<float>(v.x), sc[1] * static_cast<float>(v.y),
+                                               sc[2] * static_cast<float>(v.z), sc[3] * static_cast<float>(v.w)));
+            }
         }
     }
 }
@@ -450,12 +464,14 @@ int finish_psnr(const Geom& g, uint64_t* sse, double* psnr, cudaStream_t st) {
 int launch_quantize(const int32_t* coef, const Geom& g, const dct16a_quant& q, int32_t* qcoef,
                     float* scaled, cudaStream_t st) {
     const long long n4 = g.nblocks * 64;
-    long long grid = (n4 + 255) / 256;
-    const long long cap = static_cast<long long>(num_sms()) * 8;
-    if (grid > cap) grid = cap;
+    const long long per = 256LL * kQUnroll;
+    long long grid = static_cast<long long>(num_sms()) * 8;
+    long long chunk = (n4 + grid - 1) / grid;
+    chunk = (chunk + per - 1) / per * per;   // whole rounds: every thread keeps its 4 cells
+    grid = (n4 + chunk - 1) / chunk;
     quantize_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(
         reinterpret_cast<const int4*>(coef), reinterpret_cast<int4*>(qcoef), reinterpret_cast<float4*>(scaled),
-        n4, q.mode, q.r, q.step);
+        n4, chunk, q.mode, q.r, q.step);
     return static_cast<int>(cudaGetLastError());
 }
 
