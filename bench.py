@@ -51,6 +51,23 @@ BLOCKS_PER_IMG = (H // 16) * (W // 16)
 BYTES_PER_BLOCK = 256 + 1024          # u8 block in + int32 block out
 WORKLOAD = "config 2: 4096 x 512x512 uint8 AR(1) rho=0.95 images, forward 2-D integer transform, int32 out"
 CFG4_DISTINCT = 64
+# executed warp-instructions per unit of work of the instruction-bound kernels,
+# from the committed ncu captures (smsp__inst_executed.sum ÷ units), for the
+# issue roofline of the config entries
+ISSUE_COUNTS = {
+    "cfg3": (641.4 / 8, "profiles/r02_ncu_cfg3_band.txt: 641.4 per 8-block tile, zband_kernel<1,7>"),
+    "cfg4": (687.2 / 2, "profiles/r02_ncu_cfg4_final.txt: 556.6e6 per 810,000 block pairs, codec_warp_kernel<2,1>"),
+    "cfg5": (66.5 / 2 * 256, "profiles/r01_issue_roofline.md: 66.5 per r per block pair, sweep_kernel<1>, r = 1..256"),
+}
+
+
+def issue_roofline(name: str, blocks: int, ms: float) -> dict:
+    per, src = ISSUE_COUNTS[name]
+    achieved = per * blocks / (ms / 1e3)
+    return {"bound": "issue", "unit": "warp-instructions/s", "warp_instr_per_block": per, "achieved": achieved,
+            "peak": ISSUE_PEAK, "frac": achieved / ISSUE_PEAK,
+            "peak_source": "4 warp-instructions/clock/SM x 148 SMs x 1.965 GHz (guide SM organisation, measured max clock)",
+            "count_source": src}
 
 
 def peaks():
@@ -271,6 +288,7 @@ def leg_cfg3(c: Ctx, args, peak):
     out = {"workload": "600 x 1920x1088 u8 AR(1) video, fused zonal r=32 + recon + per-frame PSNR (valid 1080 rows)",
            "kernel": "zband_kernel<7>", "ms": ms, "blocks_per_s": blocks / ms * 1e3, "alg_bytes_per_block": 512,
            "alg_GBs": alg / ms / 1e6, "bound": "hbm", "frac": alg / ms / 1e6 / peak,
+           "issue_roofline": issue_roofline("cfg3", blocks, ms),
            "mean_psnr_db_rank0": float(psnr.mean().item())}
     return out, (x[:24].cpu().numpy() if c.rank == 0 and c.world == 1 else None)
 
@@ -341,7 +359,8 @@ def leg_cfg4(c: Ctx, args, peak):
                        "SSE all-reduce (NCCL SUM, 8 KB) + global PSNR finaliser",
            "kernel": "codec_warp_kernel<2,1>", "ms": ms, "collective_and_finaliser_ms": ms_coll,
            "blocks_per_s": blocks / ms * 1e3, "alg_bytes_per_block": 1024, "alg_GBs": alg / ms / 1e6,
-           "bound": "hbm", "frac": alg / ms / 1e6 / peak, "global_psnr_db": float(ptot.item()),
+           "bound": "hbm", "frac": alg / ms / 1e6 / peak, "issue_roofline": issue_roofline("cfg4", blocks, ms),
+           "global_psnr_db": float(ptot.item()),
            "sse_total": int(tot.item()), "sse_matches_fixtures": ok,
            "collective": f"{c.dist.get_backend()} all_reduce" if c.world > 1 else "none (1 rank)"}
     sample = distinct[:6].cpu().numpy() if c.rank == 0 and c.world == 1 else None
@@ -367,6 +386,7 @@ def leg_cfg5(c: Ctx, args, peak):
     out = {"workload": "64 x 1024x1024 u8 (rho .85/.90/.95/.98), zonal r-sweep r=1..256, SSE/PSNR per r",
            "kernel": "sweep_kernel<1>", "ms": ms, "blocks_per_s": blocks / ms * 1e3,
            "block_evals_per_s": evals / ms * 1e3, "alg_GBs": blocks * 256 / ms / 1e6, "bound": "alu (issue)",
+           "issue_roofline": issue_roofline("cfg5", blocks, ms),
            "note": "64 MiB of input, L2-resident; bounded by instruction issue, not HBM"}
     sample = None
     if c.rank == 0 and c.world == 1:   # 16 crops of 256x256 (one per rho group quarter) keep the oracle's sweep short
