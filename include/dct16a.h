@@ -301,7 +301,7 @@ DCT16A_API int dct16a_get_option(int option);
 /* Thread-local description of the calling thread's last failure ("" if none). */
 DCT16A_API const char* dct16a_last_error(void);
 
-/* Library version and build target, e.g. "dct16a 0.1.0 sm_100a". */
+/* Library version and build target, e.g. "dct16a 0.2.0 sm_100a". */
 DCT16A_API const char* dct16a_version(void);
 
 #ifdef __cplusplus

@@ -14,7 +14,7 @@ from ._lib import (OPT_CODEC_PATH, OPT_FWD_STORE, UNIFORM, ZONAL, Dct16aError, D
                    dct16a_quantize, dct16a_set_option, dct16a_sse_psnr, dct16a_ssim, dct16a_version, dct16a_zonal_sweep,
                    desc_of, lib, make_desc, make_quant)
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"
 
 
 def forward(images, out=None, stream=None):

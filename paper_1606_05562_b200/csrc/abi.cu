@@ -562,6 +562,6 @@ DCT16A_API int dct16a_get_option(int option) {
 
 DCT16A_API const char* dct16a_last_error(void) { return g_err; }
 
-DCT16A_API const char* dct16a_version(void) { return "dct16a 0.1.0 sm_100a"; }
+DCT16A_API const char* dct16a_version(void) { return "dct16a 0.2.0 sm_100a"; }
 
 }  // extern "C"
