@@ -77,7 +77,11 @@ struct ZCfg {
     static constexpr int kTuRow = kNCol == 1 ? 20 : 36;
     static constexpr int kTuBlock = kNCol == 1 ? 336 : 592;
     static constexpr int kXpose = 4 * (kTuBlock > kTyBlock ? kTuBlock : kTyBlock) * 4;
+#ifdef DCT16A_ZB_STAGES1
+    static constexpr int kStages = (ELEM == 1 && kNCol == 1) ? DCT16A_ZB_STAGES1 : 3;
+#else
     static constexpr int kStages = (ELEM == 1 && kNCol == 1) ? 4 : 3;   // TMA ring depth per warp
+#endif
     static constexpr int kStage = 16 * 128 * ELEM;                       // one tile
     static constexpr int kWarpBytes = kStages * kStage;
     // column weights (kNCol = 2): F2 [16 columns][17] (W·2^-35 for k = 0..15, DC offset)
@@ -87,7 +91,12 @@ struct ZCfg {
     // [mbarriers, per-stage tile coordinates]
     static constexpr int kSmem = 1024 + kBWarps * (kWarpBytes + kXpose) + kWtab + kBWarps * kStages * (8 + 16);
     static constexpr int kFit = (227 * 1024) / (kSmem + 1024);
-    static constexpr int kCtas = kFit < 4 ? kFit : 4;
+#ifdef DCT16A_ZB_CTAS1
+    static constexpr int kCtasMax = (ELEM == 1 && kNCol == 1) ? DCT16A_ZB_CTAS1 : 4;
+#else
+    static constexpr int kCtasMax = 4;
+#endif
+    static constexpr int kCtas = kFit < kCtasMax ? kFit : kCtasMax;
 };
 
 #ifndef DCT16A_ZB_PROMO
