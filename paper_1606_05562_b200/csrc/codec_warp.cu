@@ -2,8 +2,9 @@
 // a block pair): forward, quantisation with S folded in
 // (PAPER.md:305-344), inverse (896-901), round half away / clamp (reading A6),
 // per-image SSE (906-910).  It serves the uniform quantiser (config 4, any bit
-// depth) and the zonal cases the thread-per-block kernel does not cover
-// (10-bit, r > 36).
+// depth), the zonal cases the band kernel does not cover (r > 136) and, with
+// DCT16A_OPT_CODEC_PATH = 2, every zonal case (the GPU tests cross-check it
+// against the band kernel).
 //
 // * Data: each warp streams tiles of 8 blocks (16 rows x 128 px) through a
 //   3-stage TMA ring in the 128-byte swizzle, so the lanes of a quarter-warp
@@ -26,7 +27,8 @@
 //   networks, smem transposition in between; rounding by one round-down add
 //   onto 1.5·2^20 + 1/2 (high word = pixel, low word = fraction), clamp by one
 //   relu-min; a pixel within 2^-20 of a .5 boundary sends the warp to the exact
-//   decision (exact_row_fix → uniform_exact_floor).
+//   decision (uexact_tile.cuh: block_levels_coop → block_components_coop →
+//   exact_row_fix_levels).
 // * Zonal inverse in float32, exact (half-integers < 2^23): N + 1152.5 on the
 //   DC input, pixel = floor((N + 1152.5)/2304) by one round-down FMA; 8-bit
 //   pixels are clamped and packed by cvt.pack.sat.

@@ -90,25 +90,6 @@ __device__ __noinline__ uint32_t exact_row(const uint8_t* stage, int bb, const d
     return e;
 }
 
-// Rare branch of the uniform rounding: row t of the block has a pixel within
-// 2^-20 of a .5 boundary.  Recompute the row from the transposition tile (still
-// intact), flag the near pixels again and decide them exactly from the levels.
-template <int ELEM>
-__device__ __noinline__ void exact_row_fix(const uint8_t* stage, int bb, const double* urow, int t, int step,
-                                           int maxpix, int* pix) {
-    double rr[16], a[16];
-    for (int j = 0; j < 16; ++j) rr[j] = urow[j];
-    net_inv(rr, a);
-    int32_t qb[256];
-    exact_levels_from_stage<ELEM>(stage, bb, step, qb);
-    for (int j = 0; j < 16; ++j) {
-        bool nr;
-        int n0;
-        round_f64(a[j], nr, n0);
-        if (nr) pix[j] = min(max(uniform_exact_floor(qb, t, j, step, n0), 0), maxpix);
-    }
-}
-
 // The exact levels of one block computed by its 16 lanes together (rare
 // branch of the warp-per-block-pair codec): lane t runs the integer row
 // network on row t of the block's ORIGINAL pixels (still in the stage), the
