@@ -14,7 +14,7 @@ from oracle import codec as oc  # noqa: E402
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 100
 # the product library's kernel choices; an experiment build (DCT16A_LIB) adds 1, 3, 4
 PATHS = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 2]
-rng = np.random.default_rng(777)
+rng = np.random.default_rng(int(sys.argv[3]) if len(sys.argv) > 3 else 777)
 bad = 0
 for c in range(cases):
     bd = 8 if rng.random() < 0.5 else 10

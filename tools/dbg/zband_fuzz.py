@@ -12,7 +12,7 @@ import paper_1606_05562_b200 as pkg  # noqa: E402
 from oracle import codec as oc  # noqa: E402
 
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
-rng = np.random.default_rng(4242)
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 4242)
 bad = 0
 for c in range(cases):
     bd = 8 if rng.random() < 0.5 else 10
