@@ -218,10 +218,12 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
     const uint32_t fmask = (1u << p.F) - 1u;
 
     // per-warp transposition tiles: Y (float, row pitch 20, second block shifted 16 banks)
-    // and U (V = double/float, row pitch 17)
+    // and U (V = double, row pitch 18: 144-byte rows, so a row is read with 16-byte
+    // loads and every quarter-warp phase of them hits distinct banks; float: pitch 17)
     float* ty = reinterpret_cast<float*>(xpose) + h * (16 * 20 + 16);
     using V = typename std::conditional<UNIFORM, double, float>::type;
-    V* tu = reinterpret_cast<V*>(xpose) + h * (16 * 17);
+    constexpr int kTuP = UNIFORM ? 18 : 17;
+    V* tu = reinterpret_cast<V*>(xpose) + h * (16 * kTuP);
 
     unsigned long long acc = 0;
     int cur_n = -1;
@@ -316,15 +318,24 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
                 }
                 net_inv(c, u);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) tu[i * 17 + l] = u[i];
+                for (int i = 0; i < 16; ++i) tu[i * kTuP + l] = u[i];
             }
             __syncwarp();
             // ---- row i = t: A′[i][:] = (Tᵀ·B̂)[i][:]·T, round, clamp
             int pix[16];
             {
                 V rr[16], a[16];
+                if constexpr (UNIFORM) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) rr[j] = tu[t * 17 + j];
+                    for (int j = 0; j < 16; j += 2) {
+                        const double2 v2 = *reinterpret_cast<const double2*>(tu + t * kTuP + j);
+                        rr[j] = v2.x;
+                        rr[j + 1] = v2.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) rr[j] = tu[t * kTuP + j];
+                }
                 net_inv(rr, a);
                 if constexpr (UNIFORM) {
                     // floor(A′ + 1/2) from one round-down add (round_f64); any pixel within
@@ -343,7 +354,7 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
                         double arow[16];
                         if (nmin < 8192u) {
                             double rin[16];
-                            for (int j = 0; j < 16; ++j) rin[j] = tu[t * 17 + j];
+                            for (int j = 0; j < 16; ++j) rin[j] = tu[t * kTuP + j];
                             net_inv(rin, arow);
                         }
                         __syncwarp();
