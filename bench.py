@@ -56,7 +56,7 @@ CFG4_DISTINCT = 64
 # issue roofline of the config entries
 ISSUE_COUNTS = {
     "cfg3": (641.4 / 8, "profiles/r02_ncu_cfg3_band.txt: 641.4 per 8-block tile, zband_kernel<1,7>"),
-    "cfg4": (687.2 / 2, "profiles/r02_ncu_cfg4_final.txt: 556.6e6 per 810,000 block pairs, codec_warp_kernel<2,1>"),
+    "cfg4": (679.0 / 2, "profiles/r02_ncu_cfg4_final.txt: 550.0e6 per 810,000 block pairs, codec_warp_kernel<2,1>"),
     "cfg5": (66.5 / 2 * 256, "profiles/r01_issue_roofline.md: 66.5 per r per block pair, sweep_kernel<1>, r = 1..256"),
 }
 
