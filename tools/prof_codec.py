@@ -1,5 +1,6 @@
 """Profiling driver: N fused-codec launches on config 3 (zonal r=32) or
-config 4 (uniform, --frames frames), nothing else.  Used under ncu."""
+config 4 (uniform, --frames frames), or N r-sweeps on config 5 (--config 5:
+--frames images of 1024x1024, r = 1..256), nothing else.  Used under ncu."""
 import argparse
 import os
 import sys
@@ -16,6 +17,13 @@ ap.add_argument("--config", type=int, default=3)
 ap.add_argument("--frames", type=int, default=100)
 ap.add_argument("--launches", type=int, default=2)
 args = ap.parse_args()
+if args.config == 5:
+    x = torch.from_numpy(synth.config5_images()[:args.frames]).cuda()
+    for _ in range(args.launches):
+        pkg.zonal_sweep(x, 1, 256)
+    torch.cuda.synchronize()
+    print("ok sweep")
+    sys.exit(0)
 if args.config == 3:
     x = torch.from_numpy(synth.video_u8(args.frames)).cuda()
     q, vh = pkg.make_quant("zonal", 32), 1080
