@@ -77,6 +77,8 @@ struct ZCfg {
     static constexpr int kTuRow = kNCol == 1 ? 20 : 36;
     static constexpr int kTuBlock = kNCol == 1 ? 336 : 592;
     static constexpr int kXpose = 4 * (kTuBlock > kTyBlock ? kTuBlock : kTyBlock) * 4;
+    // DCT16A_ZB_STAGES1 / DCT16A_ZB_CTAS1: experiment knobs for the 8-bit one-column
+    // configuration (tools/dbg/zb_variants.sh, profiles/r02_band_occupancy.md)
 #ifdef DCT16A_ZB_STAGES1
     static constexpr int kStages = (ELEM == 1 && kNCol == 1) ? DCT16A_ZB_STAGES1 : 3;
 #else
