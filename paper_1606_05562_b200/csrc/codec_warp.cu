@@ -116,7 +116,27 @@ struct WParams {
     uint32_t hi_mult;   // 2^hi_shift (an opaque multiplier: one IMAD builds the high word)
     float magic_f, half_delta;
     uint32_t magic_bits;
+    // uniform, fixed-point quantiser (intq = 1): e·2^32 = |Z|·C + H exactly in 64 bits,
+    // C = round(2^32/(Δ·sqrt(G))) per cell class, H = (1/2 + δ)·2^32; window wlo
+    int intq;
+    uint32_t wlo, hfix;   // hfix < 2^32
 };
+
+// |Z| of an integer-valued float (|Z| < 2^23) as an integer: the product with
+// 2^-149 is the subnormal whose bit pattern is |Z| (exact; denormals are kept:
+// the library is built without flush-to-zero, tests/test_abi.py checks it).
+__device__ __forceinline__ uint32_t abs_z_bits(float z) { return __float_as_uint(__fmul_rn(fabsf(z), 0x1p-149f)); }
+
+// |Z|·C + H in 64 bits by one IMAD.WIDE.U32 (inline PTX: the compiler would
+// otherwise split the add of H off the multiply); returns the low word, *hi = the high word.
+__device__ __forceinline__ uint32_t mad_wide_u32(uint32_t a, uint32_t b, unsigned long long c, uint32_t* hi) {
+    unsigned long long e;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(e) : "r"(a), "r"(b), "l"(c));
+    uint32_t lo, h;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(h) : "l"(e));
+    *hi = h;
+    return lo;
+}
 
 // Exact uniform level for a coefficient whose float estimate m is flagged (rare).
 __device__ __noinline__ int32_t uniform_fix_call(float z, int32_t m, int step, int G) {
@@ -144,7 +164,9 @@ __device__ __forceinline__ void flush_sse(unsigned long long* sse, const WParams
     for (int q = 0; q < p.n_peers; ++q) atomicAdd_system(p.peers[q] + p.frame_offset + n, v);
 }
 
-template <int ELEM, bool UNIFORM>
+// FIXQ: the uniform quantiser in 64-bit fixed point (steps small enough for its
+// error bound, launch_cw); otherwise in float32
+template <int ELEM, bool UNIFORM, bool FIXQ = false>
 __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
     codec_warp_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
                       unsigned long long* __restrict__ sse, const WParams p) {
@@ -198,6 +220,7 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
     float cq[3];          // uniform: 1/(Δ·sqrt(g_k·g_l)) per class of k
     double wq[3], kq[3];  // uniform: Δ·s_k·s_l and −fl(1.5·2^E·Δ·s_k·s_l)
     uint32_t orm[3];      // uniform: all ones where the cell (k, l) is rational (never re-checked)
+    uint32_t cfix[3];     // uniform, fixed point: round(2^32/(Δ·sqrt(g_k·g_l))) per class of k
     float wz[16];         // zonal: W ⊙ M_r
     if constexpr (UNIFORM) {
         const double sl = s_of(l);
@@ -207,6 +230,7 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
             const int kk = c == 0 ? 0 : (c == 1 ? 2 : 3);   // representatives of g = 16, 12, 8
             const double s = s_of(kk) * sl;
             cq[c] = static_cast<float>(s / p.step);
+            cfix[c] = static_cast<uint32_t>(__double2ull_rn(ldexp(s / p.step, 32)));
             wq[c] = static_cast<double>(p.step) * s;
             kq[c] = -(Kmag * wq[c]);
             orm[c] = c == cl ? 0xFFFFFFFFu : 0u;
@@ -279,35 +303,75 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
             {
                 V c[16], u[16];
                 if constexpr (UNIFORM) {
-                    // level m = floor(e), e = |Z|·c + 1/2 + δ, from the bits of one
-                    // round-down add onto 1.5·2^(23-F): bits >> F = (magic >> F) + m and the
-                    // low F bits are the fraction.  The high word of the double 1.5·2^E + m
-                    // is one IMAD of bits >> F; the sign of Z flips the DFMA result.
+                    // level m = floor(e), e = |Z|·c + 1/2 + δ.  δ (> the evaluation error,
+                    // below the 1/(32Δ) spacing of the rational cells) makes the rational
+                    // cells — the only ones with exact ties — exact; an irrational cell whose
+                    // fraction falls in the window [0, δ + 2·err) is re-decided in integers.
+                    // The level enters the float64 inverse as the double 1.5·2^E + m (its
+                    // high word one IMAD of m) times the weight by one DFMA; the sign of Z
+                    // flips the result's sign bit.
                     uint32_t nmin = 0xFFFFFFFFu;
+                    if constexpr (FIXQ) {
+                        const unsigned long long hfix64 = p.hfix;
+                        // fixed point: |Z|·C + H = (e + error)·2^32 exactly in 64 bits (one
+                        // IMAD.WIDE), C = round(2^32·c), H = (1/2 + δ)·2^32: m is the high
+                        // word, the fraction the low word
 #pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        const int ck = uclass(k);
-                        const float e = fmaf(fabsf(z[k]), cq[ck], p.half_delta);
-                        const uint32_t bits = __float_as_uint(__fadd_rd(e, p.magic_f));
-                        nmin = min(nmin, (bits & fmask) | orm[ck]);
-                        const double d = __hiloint2double(static_cast<int>((bits >> p.F) * p.hi_mult + p.hi_c2), 0);
-                        const double cm = fma(d, wq[ck], kq[ck]);
-                        c[k] = __hiloint2double(__double2hiint(cm) ^ static_cast<int>(__float_as_uint(z[k]) & 0x80000000u),
-                                                __double2loint(cm));
-                    }
-                    // irrational cell with its fraction in the window [0, δ + 2·err): decide exactly
-                    if (__any_sync(0xffffffffu, nmin < static_cast<uint32_t>(p.wbits))) {
+                        for (int k = 0; k < 16; ++k) {
+                            const int ck = uclass(k);
+                            const uint32_t az = abs_z_bits(z[k]);
+                            uint32_t m;
+                            const uint32_t fr = mad_wide_u32(az, cfix[ck], hfix64, &m);
+                            nmin = min(nmin, fr | orm[ck]);
+                            const double d = __hiloint2double(static_cast<int>(m * p.hi_mult + p.hi_c), 0);
+                            const double cm = fma(d, wq[ck], kq[ck]);
+                            c[k] = __hiloint2double(__double2hiint(cm) ^ static_cast<int>(__float_as_uint(z[k]) & 0x80000000u),
+                                                    __double2loint(cm));
+                        }
+                        if (__any_sync(0xffffffffu, nmin < p.wlo)) {
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) {
+                                const int ck = uclass(k);
+                                const uint32_t az = abs_z_bits(z[k]);
+                                uint32_t m0;
+                                const uint32_t fr = mad_wide_u32(az, cfix[ck], hfix64, &m0);
+                                if ((fr | orm[ck]) < p.wlo) {
+                                    const int32_t m = uniform_fix(az, static_cast<int32_t>(m0),
+                                                                  static_cast<uint64_t>(p.step) * p.step * (g_of(k) * g_of(l)));
+                                    const double d = __hiloint2double((m << p.hi_shift) + p.hi_c, 0);
+                                    const double cm = fma(d, wq[ck], kq[ck]);
+                                    c[k] = z[k] < 0.0f ? -cm : cm;
+                                }
+                            }
+                        }
+                    } else {
+                        // float32 (steps too large for the fixed point's error bound): one FMA
+                        // and one round-down magic add onto 1.5·2^(23-F) keeping F fraction bits
 #pragma unroll
                         for (int k = 0; k < 16; ++k) {
                             const int ck = uclass(k);
                             const float e = fmaf(fabsf(z[k]), cq[ck], p.half_delta);
                             const uint32_t bits = __float_as_uint(__fadd_rd(e, p.magic_f));
-                            if (((bits & fmask) | orm[ck]) < static_cast<uint32_t>(p.wbits)) {
-                                const int32_t m = uniform_fix_call(z[k], static_cast<int32_t>((bits - p.magic_bits) >> p.F),
-                                                                   p.step, g_of(k) * g_of(l));
-                                const double d = __hiloint2double((m << p.hi_shift) + p.hi_c, 0);
-                                const double cm = fma(d, wq[ck], kq[ck]);
-                                c[k] = z[k] < 0.0f ? -cm : cm;
+                            nmin = min(nmin, (bits & fmask) | orm[ck]);
+                            const double d = __hiloint2double(static_cast<int>((bits >> p.F) * p.hi_mult + p.hi_c2), 0);
+                            const double cm = fma(d, wq[ck], kq[ck]);
+                            c[k] = __hiloint2double(__double2hiint(cm) ^ static_cast<int>(__float_as_uint(z[k]) & 0x80000000u),
+                                                    __double2loint(cm));
+                        }
+                        // irrational cell with its fraction in the window [0, δ + 2·err): decide exactly
+                        if (__any_sync(0xffffffffu, nmin < static_cast<uint32_t>(p.wbits))) {
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) {
+                                const int ck = uclass(k);
+                                const float e = fmaf(fabsf(z[k]), cq[ck], p.half_delta);
+                                const uint32_t bits = __float_as_uint(__fadd_rd(e, p.magic_f));
+                                if (((bits & fmask) | orm[ck]) < static_cast<uint32_t>(p.wbits)) {
+                                    const int32_t m = uniform_fix_call(z[k], static_cast<int32_t>((bits - p.magic_bits) >> p.F),
+                                                                       p.step, g_of(k) * g_of(l));
+                                    const double d = __hiloint2double((m << p.hi_shift) + p.hi_c, 0);
+                                    const double cm = fma(d, wq[ck], kq[ck]);
+                                    c[k] = z[k] < 0.0f ? -cm : cm;
+                                }
                             }
                         }
                     }
@@ -505,8 +569,26 @@ int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon
         p.hi_c = 0x3FF00000 + ((E) << 20) + (1 << 19);   // high word of 1.5·2^E
         // the same word from bits >> F = (magic_bits >> F) + m (arithmetic mod 2^32)
         p.hi_c2 = static_cast<int>(static_cast<uint32_t>(p.hi_c) - ((p.magic_bits >> p.F) << p.hi_shift));
+        // fixed point: C = round(2^32·c) from a double within 2^-20 of 2^32·c, so |C − 2^32·c| <= 0.501 and
+        // |Z|·C + H = (e + ε)·2^32 with |ε| <= err_fx; usable while δ > err_fx and δ + err_fx < 1/(32Δ)
+        const double az_max = 256.0 * p.maxpix;
+        const double err_fx = (az_max * 0.501 + 1.0) * 0x1p-32;
+        const unsigned long long H = static_cast<unsigned long long>(llround(ldexp(0.5 + 2.0 * err_fx, 32)));
+        const double dfx = ldexp(static_cast<double>(H), -32) - 0.5;
+        const double wlo = ceil(ldexp(dfx + 2.0 * err_fx, 32));
+        // taken for steps <= 6 only: there the float path's window flags many coefficients
+        // (Δ = 1..6: 5.0-6.0 ms against 4.25-4.3 ms per 300 config-4 frames), while at
+        // Δ >= 7 the float path is as fast or faster (Δ = 16: 3.96 against 4.22 ms;
+        // profiles/r02_config4_packed_lanes.md)
+        p.intq = q.step <= 6 && dfx > err_fx && dfx + err_fx < 1.0 / (32.0 * q.step) && wlo < 4294967296.0 ? 1 : 0;
+        p.hfix = static_cast<uint32_t>(H);   // (1/2 + δ)·2^32 < 2^32
+        p.wlo = p.intq ? static_cast<uint32_t>(wlo) : 0u;
     }
-    if (int e = smem_optin(reinterpret_cast<const void*>(codec_warp_kernel<ELEM, UNIFORM>), Cfg::kSmem)) return e;
+    void (*kern)(const CUtensorMap, const CUtensorMap, unsigned long long*, const WParams) =
+        codec_warp_kernel<ELEM, UNIFORM, false>;
+    if constexpr (UNIFORM)
+        if (p.intq) kern = codec_warp_kernel<ELEM, UNIFORM, true>;
+    if (int e = smem_optin(reinterpret_cast<const void*>(kern), Cfg::kSmem)) return e;
     long long grid = static_cast<long long>(num_sms()) * Cfg::kCtasPerSm;
     // runs of up to kWClaim tiles, shorter when there are few tiles per resident warp
     // (a small batch then still spreads over many warps)
@@ -517,8 +599,8 @@ int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon
     SchedGuard guard(kSchedCodecWarp, st);
     if (guard.error()) return guard.error();
     p.slot = guard.slot();
-    codec_warp_kernel<ELEM, UNIFORM><<<static_cast<unsigned>(grid), kWWarps * 32, Cfg::kSmem, st>>>(
-        tin, tout, reinterpret_cast<unsigned long long*>(sse), p);
+    kern<<<static_cast<unsigned>(grid), kWWarps * 32, Cfg::kSmem, st>>>(tin, tout,
+                                                                        reinterpret_cast<unsigned long long*>(sse), p);
     return static_cast<int>(cudaGetLastError());
 }
 

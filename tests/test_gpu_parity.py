@@ -267,10 +267,11 @@ def test_codec_without_recon_output(codec_path):
     assert sse.cpu().tolist() == oc.codec_images(f, "uniform", step=16, bit_depth=10)["sse"]
 
 
-@pytest.mark.parametrize("step", [1, 3, 16, 24, 200, 65535])
+@pytest.mark.parametrize("step", [1, 2, 3, 4, 5, 6, 7, 16, 24, 200, 65535])
 @pytest.mark.parametrize("shape", [(1, 16, 16), (2, 48, 208), (1, 32, 1920)])
 def test_codec_uniform_steps_and_shapes(step, shape, codec_path):
-    """Uniform codec (warp kernel) for small to huge steps, a single block, a
+    """Uniform codec (warp kernel) for small to huge steps — Δ <= 6 takes the
+    fixed-point quantiser, larger steps the float one — a single block, a
     ragged tile (13 blocks per strip) and a wide strip, 10-bit and 8-bit."""
     n, h, w = shape
     f = synth.frames_10bit(list(range(20, 20 + n)), H=h, W=w, workers=1)
@@ -641,7 +642,7 @@ def test_forward_every_store_mode(mode):
         pkg.dct16a_set_option(pkg.OPT_FWD_STORE, old)
 
 
-@pytest.mark.parametrize("step", [8, 24, 40, 72])
+@pytest.mark.parametrize("step", [2, 4, 6, 8, 24, 40, 72])
 def test_codec_uniform_reconstruction_ties(step, codec_path):
     """Flat blocks: only the DC level survives, A′ = Δ·q00/16, an exact .5 tie
     whenever Δ·q00 ≡ 8 (mod 16) — the fused kernel must send those pixels to

@@ -15,6 +15,7 @@ cases = int(sys.argv[1]) if len(sys.argv) > 1 else 100
 # the product library's kernel choices; an experiment build (DCT16A_LIB) adds 1, 3, 4
 PATHS = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 2]
 rng = np.random.default_rng(int(sys.argv[3]) if len(sys.argv) > 3 else 777)
+MAXSTEP = int(sys.argv[4]) if len(sys.argv) > 4 else 119   # uniform steps drawn from [1, MAXSTEP]
 bad = 0
 for c in range(cases):
     bd = 8 if rng.random() < 0.5 else 10
@@ -33,7 +34,7 @@ for c in range(cases):
     mode = "zonal" if rng.random() < 0.5 else "uniform"
     u = rng.random()
     r = int(rng.integers(1, 257)) if u < 0.3 else (int(rng.integers(1, 37)) if u < 0.6 else int(rng.integers(37, 137)))
-    step = int(rng.integers(1, 120))
+    step = int(rng.integers(1, MAXSTEP + 1))
     vh = int(rng.integers(1, H + 1)) if rng.random() < 0.3 else None
     ref = oc.codec_images(view, mode, r=r, step=step, bit_depth=bd, valid_height=vh)
     for path in PATHS:
