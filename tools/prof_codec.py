@@ -16,6 +16,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=3)
 ap.add_argument("--frames", type=int, default=100)
 ap.add_argument("--launches", type=int, default=2)
+ap.add_argument("--step", type=int, default=16, help="config 4: uniform step")
 args = ap.parse_args()
 if args.config == 5:
     x = torch.from_numpy(synth.config5_images()[:args.frames]).cuda()
@@ -29,7 +30,7 @@ if args.config == 3:
     q, vh = pkg.make_quant("zonal", 32), 1080
 else:
     x = torch.from_numpy(synth.frames_10bit(range(args.frames))).cuda()
-    q, vh = pkg.make_quant("uniform", step=16), None
+    q, vh = pkg.make_quant("uniform", step=args.step), None
 n = x.shape[0]
 recon = torch.empty_like(x)
 sse = torch.empty(n, dtype=torch.int64, device="cuda")
