@@ -546,21 +546,25 @@ int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon
     p.r = q.r;
     p.step = q.step;
     if (UNIFORM) {
-        // e = |Z|/(Δ·sqrt(G)) + 1/2 <= e_max; float error <= e_max·2^-23 (rounded c
-        // and the fma); δ = 2·err keeps the rational cells exact because
-        // δ + err < 1/(32Δ), the smallest spacing of their e (reading A9).
+        // e = |Z|/(Δ·sqrt(G)) + 1/2 <= e_max (|Z| <= maxpix·g_k·g_l); the float
+        // evaluation e' = e + δ + ε has |ε| <= err = e_max·2^-23 (the rounded c and
+        // the fma).  With δ > err, e' > e, so a rational cell's exact tie (e an
+        // integer) rounds up as it must and, because δ + err < 1/(32Δ) (the
+        // smallest spacing of their e, reading A9), no other rational value crosses
+        // an integer; an irrational cell's level is one too high only when the
+        // fraction of e' is below δ + err: the window (δ = 1.25·err).
         const double e_max = 16.0 * p.maxpix / q.step + 1.0;
         const double err = e_max * 0x1p-23;
         int nbits = 0;
         while ((1 << nbits) <= static_cast<int>(e_max) + 1) ++nbits;
         p.F = 22 - nbits;
-        const float hd = static_cast<float>(0.5 + 2.0 * err);
+        const float hd = static_cast<float>(0.5 + 1.25 * err);
         const double delta = static_cast<double>(hd) - 0.5;
         if (!(delta > err && delta + err < 1.0 / (32.0 * q.step))) return DCT16A_EDOMAIN;
         p.half_delta = hd;
         p.magic_f = 1.5f * static_cast<float>(1 << (23 - p.F));
         memcpy(&p.magic_bits, &p.magic_f, 4);
-        p.wbits = static_cast<int>(ceil((delta + 2.0 * err) * (1 << p.F)));
+        p.wbits = static_cast<int>(ceil((delta + err) * (1 << p.F)));
         // level -> double 1.5·2^E + m: E with 2^E > 2·m_max, m placed at bit (20 - E) of the high word
         int E = 1;
         while ((1 << E) <= 2 * (static_cast<int>(e_max) + 1)) ++E;
@@ -573,9 +577,9 @@ int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon
         // |Z|·C + H = (e + ε)·2^32 with |ε| <= err_fx; usable while δ > err_fx and δ + err_fx < 1/(32Δ)
         const double az_max = 256.0 * p.maxpix;
         const double err_fx = (az_max * 0.501 + 1.0) * 0x1p-32;
-        const unsigned long long H = static_cast<unsigned long long>(llround(ldexp(0.5 + 2.0 * err_fx, 32)));
+        const unsigned long long H = static_cast<unsigned long long>(llround(ldexp(0.5 + 1.25 * err_fx, 32)));
         const double dfx = ldexp(static_cast<double>(H), -32) - 0.5;
-        const double wlo = ceil(ldexp(dfx + 2.0 * err_fx, 32));
+        const double wlo = ceil(ldexp(dfx + err_fx, 32));
         // taken for steps <= 6 only: there the float path's window flags many coefficients
         // (Δ = 1..6: 5.0-6.0 ms against 4.25-4.3 ms per 300 config-4 frames), while at
         // Δ >= 7 the float path is as fast or faster (Δ = 16: 3.96 against 4.22 ms;
