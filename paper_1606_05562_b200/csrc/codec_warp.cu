@@ -144,6 +144,39 @@ __device__ __noinline__ int32_t uniform_fix_call(float z, int32_t m, int step, i
     return uniform_fix(az, m, static_cast<uint64_t>(step) * step * G);
 }
 
+// The rare re-decision of a lane's flagged coefficients (bit k of `flagged`: the
+// fraction of coefficient k's level estimate lies in the window), kept compact
+// for the instruction cache: a rolled loop over the flagged k only, the exact
+// level by uniform_fix (from a float estimate; it corrects by one step), the
+// new input of the float64 inverse into a per-lane slot of the warp's
+// transposition tile (free between the column pass and the inverse), then the
+// flagged registers reloaded.  The whole warp calls it (it synchronises).
+__device__ __forceinline__ void refix_levels(uint32_t flagged, const float (&z)[16], double (&c)[16], uint8_t* xpose,
+                                          int lane, const float (&cq)[3], const double (&wq)[3],
+                                          const double (&kq)[3], int l, const WParams& p) {
+    double* slot = reinterpret_cast<double*>(xpose) + lane * 16;
+    const int gl = g_of(l);
+    for (uint32_t f = flagged; f; f &= f - 1) {
+        const int k = __ffs(f) - 1;
+        float zk = 0.0f;
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) zk = kk == k ? z[kk] : zk;
+        const int ck = uclass(k);
+        const float cqk = ck == 0 ? cq[0] : (ck == 1 ? cq[1] : cq[2]);
+        const double wqk = ck == 0 ? wq[0] : (ck == 1 ? wq[1] : wq[2]);
+        const double kqk = ck == 0 ? kq[0] : (ck == 1 ? kq[1] : kq[2]);
+        const uint32_t az = static_cast<uint32_t>(fabsf(zk));
+        const int32_t m0 = static_cast<int32_t>(fmaf(static_cast<float>(az), cqk, 0.5f));   // within one of the level
+        const int32_t m = uniform_fix(az, m0, static_cast<uint64_t>(p.step) * p.step * (g_of(k) * gl));
+        const double cm = fma(__hiloint2double((m << p.hi_shift) + p.hi_c, 0), wqk, kqk);
+        slot[k] = zk < 0.0f ? -cm : cm;
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+        if (flagged & (1u << k)) c[k] = slot[k];
+    __syncwarp();   // the slots are the transposition tile the inverse writes next
+}
+
 }  // namespace
 
 // Add one image's SSE: locally, or into every rank's vector — with one
@@ -329,20 +362,14 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
                                                     __double2loint(cm));
                         }
                         if (__any_sync(0xffffffffu, nmin < p.wlo)) {
+                            uint32_t flagged = 0;
 #pragma unroll
                             for (int k = 0; k < 16; ++k) {
-                                const int ck = uclass(k);
-                                const uint32_t az = abs_z_bits(z[k]);
                                 uint32_t m0;
-                                const uint32_t fr = mad_wide_u32(az, cfix[ck], hfix64, &m0);
-                                if ((fr | orm[ck]) < p.wlo) {
-                                    const int32_t m = uniform_fix(az, static_cast<int32_t>(m0),
-                                                                  static_cast<uint64_t>(p.step) * p.step * (g_of(k) * g_of(l)));
-                                    const double d = __hiloint2double((m << p.hi_shift) + p.hi_c, 0);
-                                    const double cm = fma(d, wq[ck], kq[ck]);
-                                    c[k] = z[k] < 0.0f ? -cm : cm;
-                                }
+                                const uint32_t fr = mad_wide_u32(abs_z_bits(z[k]), cfix[uclass(k)], hfix64, &m0);
+                                if ((fr | orm[uclass(k)]) < p.wlo) flagged |= 1u << k;
                             }
+                            refix_levels(flagged, z, c, xpose, lane, cq, wq, kq, l, p);
                         }
                     } else {
                         // float32 (steps too large for the fixed point's error bound): one FMA
@@ -360,19 +387,14 @@ __global__ void __launch_bounds__(kWWarps * 32, WCfg<ELEM, UNIFORM>::kCtasPerSm)
                         }
                         // irrational cell with its fraction in the window [0, δ + 2·err): decide exactly
                         if (__any_sync(0xffffffffu, nmin < static_cast<uint32_t>(p.wbits))) {
+                            uint32_t flagged = 0;   // the lane's coefficients in the window
 #pragma unroll
                             for (int k = 0; k < 16; ++k) {
-                                const int ck = uclass(k);
-                                const float e = fmaf(fabsf(z[k]), cq[ck], p.half_delta);
+                                const float e = fmaf(fabsf(z[k]), cq[uclass(k)], p.half_delta);
                                 const uint32_t bits = __float_as_uint(__fadd_rd(e, p.magic_f));
-                                if (((bits & fmask) | orm[ck]) < static_cast<uint32_t>(p.wbits)) {
-                                    const int32_t m = uniform_fix_call(z[k], static_cast<int32_t>((bits - p.magic_bits) >> p.F),
-                                                                       p.step, g_of(k) * g_of(l));
-                                    const double d = __hiloint2double((m << p.hi_shift) + p.hi_c, 0);
-                                    const double cm = fma(d, wq[ck], kq[ck]);
-                                    c[k] = z[k] < 0.0f ? -cm : cm;
-                                }
+                                if (((bits & fmask) | orm[uclass(k)]) < static_cast<uint32_t>(p.wbits)) flagged |= 1u << k;
                             }
+                            refix_levels(flagged, z, c, xpose, lane, cq, wq, kq, l, p);
                         }
                     }
                 } else {

@@ -112,22 +112,28 @@ __device__ __noinline__ bool block_levels_coop(const uint8_t* stage, int bb, int
     }
     __syncwarp();
     const int l = t;
-    int32_t c[16], z[16];
-    for (int k = 0; k < 16; ++k) c[k] = qs[k * 20 + l];
-    net_fwd(c, z);
-    __syncwarp();   // every lane has read its column before the levels overwrite the tile
+    {
+        int32_t c[16], z[16];
+        for (int k = 0; k < 16; ++k) c[k] = qs[k * 20 + l];
+        net_fwd(c, z);
+        __syncwarp();   // every lane has read its column before Z overwrites the tile
+        for (int k = 0; k < 16; ++k) qs[k * 20 + l] = z[k];
+    }
     bool irr = false;
     const float rstep = 1.0f / static_cast<float>(step);
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        const uint32_t az = static_cast<uint32_t>(z[k] < 0 ? -z[k] : z[k]);
-        const int G = g_of(k) * g_of(l);
+    const int gl = g_of(l);
+#pragma unroll 1
+    for (int k = 0; k < 16; ++k) {   // rolled: this rare branch is kept small (instruction cache)
+        const int32_t zk = qs[k * 20 + l];
+        const uint32_t az = static_cast<uint32_t>(zk < 0 ? -zk : zk);
+        const int gk = g_of(k);
+        const int G = gk * gl;
         const uint64_t d2g = static_cast<uint64_t>(step) * step * G;
         // a float estimate within one of the level; uniform_fix makes it exact
         const float e = static_cast<float>(az) * rsqrtf(static_cast<float>(G)) * rstep + 0.5f;
         const int32_t m = uniform_fix(az, static_cast<int32_t>(e), d2g);
-        qs[k * 20 + l] = z[k] < 0 ? -m : m;
-        irr |= m != 0 && g_of(k) != g_of(l);
+        qs[k * 20 + l] = zk < 0 ? -m : m;
+        irr |= m != 0 && gk != gl;
     }
     __syncwarp();
     return irr;
@@ -154,8 +160,8 @@ __device__ __noinline__ void block_components_coop(const int32_t* qs, int32_t* u
         // J1 rational, J2 classes (16, 8): √2, J3 (16, 12): √3, J6 (12, 8): √6
         comp[k] = ck == cl ? 0 : (ck + cl == 2 ? 1 : (ck + cl == 1 ? 2 : 3));
     }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {   // rolled (rare branch, instruction cache); J is in local memory
         int32_t w[16], u[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) w[k] = comp[k] == c ? wk[k] : 0;
