@@ -11,12 +11,15 @@
 
 namespace dct16a {
 
-__host__ __device__ constexpr int g_of(int k) {
-    // 1/S_kk² from PAPER.md:315-329: 1/4 -> 16, 1/sqrt(12) -> 12, 1/sqrt(8) -> 8
-    return k == 0 || k == 1 || k == 5 || k == 8 ? 16
-         : (k == 3 || k == 4 || k == 11 || k == 12) ? 8
-                                                    : 12;
-}
+// 1/S_kk² from PAPER.md:315-329: 1/4 -> 16 (k = 0, 1, 5, 8), 1/sqrt(12) -> 12,
+// 1/sqrt(8) -> 8 (k = 3, 4, 11, 12), as the class c_k = (16 - g_k)/4 in two bits
+// per k (branch-free for a runtime k: one shift, one mask)
+constexpr uint32_t kGClassBits = 0x56945290u;
+__host__ __device__ constexpr int g_class(int k) { return static_cast<int>((kGClassBits >> (2 * k)) & 3u); }
+__host__ __device__ constexpr int g_of(int k) { return 16 - 4 * g_class(k); }
+static_assert(g_of(0) == 16 && g_of(1) == 16 && g_of(5) == 16 && g_of(8) == 16 && g_of(3) == 8 &&
+                  g_of(4) == 8 && g_of(11) == 8 && g_of(12) == 8 && g_of(2) == 12 && g_of(15) == 12,
+              "g_k of PAPER.md:315-329");
 
 // rank of (k, l) in the 16x16 zig-zag scan (0 = DC, 255 = (15,15))
 __host__ __device__ constexpr int zigzag_rank(int k, int l) {

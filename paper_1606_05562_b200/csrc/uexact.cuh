@@ -22,7 +22,7 @@
 
 namespace dct16a {
 
-__device__ __forceinline__ int uclass(int k) { return g_of(k) == 16 ? 0 : (g_of(k) == 12 ? 1 : 2); }
+__device__ __forceinline__ int uclass(int k) { return g_class(k); }   // 0, 1, 2 for g = 16, 12, 8
 
 // sign(a + b·√2), exact
 __device__ __forceinline__ int sign_r2(__int128 a, __int128 b) {

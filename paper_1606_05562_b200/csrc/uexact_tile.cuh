@@ -129,9 +129,15 @@ __device__ __noinline__ bool block_levels_coop(const uint8_t* stage, int bb, int
         const int gk = g_of(k);
         const int G = gk * gl;
         const uint64_t d2g = static_cast<uint64_t>(step) * step * G;
-        // a float estimate within one of the level; uniform_fix makes it exact
+        // a float estimate (error < e·2^-21: rsqrtf within 2 ulp, two roundings); it
+        // is the level unless its fraction lies within e·2^-20 of an integer, where
+        // uniform_fix decides exactly (it corrects by one step)
         const float e = static_cast<float>(az) * rsqrtf(static_cast<float>(G)) * rstep + 0.5f;
-        const int32_t m = uniform_fix(az, static_cast<int32_t>(e), d2g);
+        const float fl = floorf(e);
+        const float fr = e - fl;
+        const float mg = fmaf(e, 0x1p-20f, 0x1p-20f);
+        int32_t m = static_cast<int32_t>(fl);
+        if (fr < mg || fr > 1.0f - mg) m = uniform_fix(az, m, d2g);
         qs[k * 20 + l] = zk < 0 ? -m : m;
         irr |= m != 0 && gk != gl;
     }
