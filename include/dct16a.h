@@ -290,11 +290,17 @@ DCT16A_API int64_t dct16a_forward_host_workspace(const dct16a_desc* desc, int32_
  *     kernel, -1 = default (5 for 8-bit, 3 for 10-bit), 3 = 8 KB TMA stores,
  *     5 = one 32 KB TMA store per tile (experiment builds: 0..7, the variants
  *     of profiles/r01_fwd_store_modes.md).
+ *   DCT16A_OPT_UNIFORM_QUANT (env DCT16A_UNIFORM_QUANT): the fused codec's
+ *     uniform quantiser (reading A9; both decide every level exactly),
+ *     0 = automatic (default): 64-bit fixed point for steps <= 8, float32 above;
+ *     1 = always float32; 2 = fixed point wherever its error bound allows it
+ *     (steps up to ~170 for 10-bit, ~680 for 8-bit input), float32 beyond.
  * A value the library was not built with returns DCT16A_EDOMAIN (from the
  * environment it is ignored).
  */
-#define DCT16A_OPT_CODEC_PATH 1
-#define DCT16A_OPT_FWD_STORE  2
+#define DCT16A_OPT_CODEC_PATH    1
+#define DCT16A_OPT_FWD_STORE     2
+#define DCT16A_OPT_UNIFORM_QUANT 3
 DCT16A_API int dct16a_set_option(int option, int value);
 DCT16A_API int dct16a_get_option(int option);
 

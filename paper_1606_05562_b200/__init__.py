@@ -8,7 +8,7 @@ memory, streams and process groups only.
 """
 from __future__ import annotations
 
-from ._lib import (OPT_CODEC_PATH, OPT_FWD_STORE, UNIFORM, ZONAL, Dct16aError, Desc, Quant,  # noqa: F401
+from ._lib import (OPT_CODEC_PATH, OPT_FWD_STORE, OPT_UNIFORM_QUANT, UNIFORM, ZONAL, Dct16aError, Desc, Quant,  # noqa: F401
                    dct16a_codec, dct16a_codec_allreduce, dct16a_forward, dct16a_forward16, dct16a_forward_host,
                    dct16a_forward_host_workspace, dct16a_get_option, dct16a_inverse, dct16a_last_error, dct16a_psnr,
                    dct16a_quantize, dct16a_set_option, dct16a_sse_psnr, dct16a_ssim, dct16a_version, dct16a_zonal_sweep,

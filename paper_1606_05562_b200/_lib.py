@@ -18,6 +18,7 @@ ZONAL = 0
 UNIFORM = 1
 OPT_CODEC_PATH = 1
 OPT_FWD_STORE = 2
+OPT_UNIFORM_QUANT = 3
 
 ERRORS = {-1: "ENULL", -2: "ESHAPE", -3: "EPITCH", -4: "EALIGN", -5: "EDOMAIN", -6: "ECUDA"}
 
@@ -319,6 +320,6 @@ def dct16a_set_option(option: int, value: int) -> None:
 
 def dct16a_get_option(option: int) -> int:
     v = lib().dct16a_get_option(option)
-    if option not in (OPT_CODEC_PATH, OPT_FWD_STORE):
+    if option not in (OPT_CODEC_PATH, OPT_FWD_STORE, OPT_UNIFORM_QUANT):
         _check(v)
     return v

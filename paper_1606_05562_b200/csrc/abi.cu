@@ -168,11 +168,14 @@ int env_option(const char* name, int dflt, bool (*ok)(int)) {
 }
 std::atomic<int> g_codec_path{env_option("DCT16A_CODEC_PATH", 0, codec_path_built)};
 std::atomic<int> g_fwd_store{env_option("DCT16A_FWD_STORE", -1, store_mode_built)};
+bool uniform_quant_valid(int v) { return v >= 0 && v <= 2; }
+std::atomic<int> g_uniform_quant{env_option("DCT16A_UNIFORM_QUANT", 0, uniform_quant_valid)};
 }  // namespace
 
 int get_option(int option) {
     if (option == DCT16A_OPT_CODEC_PATH) return g_codec_path.load(std::memory_order_relaxed);
     if (option == DCT16A_OPT_FWD_STORE) return g_fwd_store.load(std::memory_order_relaxed);
+    if (option == DCT16A_OPT_UNIFORM_QUANT) return g_uniform_quant.load(std::memory_order_relaxed);
     return 0;
 }
 
@@ -551,11 +554,16 @@ DCT16A_API int dct16a_set_option(int option, int value) {
         g_fwd_store.store(value);
         return DCT16A_OK;
     }
+    if (option == DCT16A_OPT_UNIFORM_QUANT) {
+        if (!uniform_quant_valid(value)) return fail(DCT16A_EDOMAIN, "uniform quantiser choice %d not in {0, 1, 2}", value);
+        g_uniform_quant.store(value);
+        return DCT16A_OK;
+    }
     return fail(DCT16A_EDOMAIN, "unknown option %d", option);
 }
 
 DCT16A_API int dct16a_get_option(int option) {
-    if (option != DCT16A_OPT_CODEC_PATH && option != DCT16A_OPT_FWD_STORE)
+    if (option != DCT16A_OPT_CODEC_PATH && option != DCT16A_OPT_FWD_STORE && option != DCT16A_OPT_UNIFORM_QUANT)
         return fail(DCT16A_EDOMAIN, "unknown option %d", option);
     return get_option(option);
 }

@@ -602,11 +602,13 @@ int launch_cw(const void* src, const Geom& g, const dct16a_quant& q, void* recon
         const unsigned long long H = static_cast<unsigned long long>(llround(ldexp(0.5 + 1.25 * err_fx, 32)));
         const double dfx = ldexp(static_cast<double>(H), -32) - 0.5;
         const double wlo = ceil(ldexp(dfx + err_fx, 32));
-        // taken for steps <= 6 only: there the float path's window flags many coefficients
-        // (Δ = 1..6: 5.0-6.0 ms against 4.25-4.3 ms per 300 config-4 frames), while at
-        // Δ >= 7 the float path is as fast or faster (Δ = 16: 3.96 against 4.22 ms;
-        // profiles/r02_config4_packed_lanes.md)
-        p.intq = q.step <= 6 && dfx > err_fx && dfx + err_fx < 1.0 / (32.0 * q.step) && wlo < 4294967296.0 ? 1 : 0;
+        // automatic choice: fixed point for steps <= 8, where the float window flags
+        // many coefficients (Δ = 1..8: 4.0-5.0 ms float against 4.04-4.08 fixed per 300
+        // config-4 frames); above, the float path is 1-2 % faster at most steps
+        // (Δ = 16: 3.95 against 4.03 ms; profiles/r02_config4_packed_lanes.md)
+        const int choice = get_option(DCT16A_OPT_UNIFORM_QUANT);   // 0 auto, 1 float, 2 fixed point
+        const bool fx_ok = dfx > err_fx && dfx + err_fx < 1.0 / (32.0 * q.step) && wlo < 4294967296.0;
+        p.intq = fx_ok && (choice == 2 || (choice == 0 && q.step <= 8)) ? 1 : 0;
         p.hfix = static_cast<uint32_t>(H);   // (1/2 + δ)·2^32 < 2^32
         p.wlo = p.intq ? static_cast<uint32_t>(wlo) : 0u;
     }

@@ -126,6 +126,15 @@ def test_options_validate_and_round_trip():
     for bad in (0, 1, 2, 4, 6, 7, 8):
         with pytest.raises(pkg.Dct16aError):
             pkg.dct16a_set_option(pkg.OPT_FWD_STORE, bad)
+    old = pkg.dct16a_get_option(pkg.OPT_UNIFORM_QUANT)
+    assert old == 0
+    for v in (0, 1, 2):
+        pkg.dct16a_set_option(pkg.OPT_UNIFORM_QUANT, v)
+        assert pkg.dct16a_get_option(pkg.OPT_UNIFORM_QUANT) == v
+    pkg.dct16a_set_option(pkg.OPT_UNIFORM_QUANT, old)
+    for bad in (-1, 3):
+        with pytest.raises(pkg.Dct16aError):
+            pkg.dct16a_set_option(pkg.OPT_UNIFORM_QUANT, bad)
     with pytest.raises(pkg.Dct16aError) as e:
         pkg.dct16a_set_option(99, 0)
     assert e.value.code == -5

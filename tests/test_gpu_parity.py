@@ -267,6 +267,26 @@ def test_codec_without_recon_output(codec_path):
     assert sse.cpu().tolist() == oc.codec_images(f, "uniform", step=16, bit_depth=10)["sse"]
 
 
+@pytest.fixture(params=[0, 1, 2], ids=["quant-auto", "quant-float", "quant-fixed"])
+def uniform_quant(request):
+    """Every uniform case on each quantiser choice (DCT16A_OPT_UNIFORM_QUANT):
+    automatic, always float32, fixed point wherever its bound allows."""
+    old = pkg.dct16a_get_option(pkg.OPT_UNIFORM_QUANT)
+    pkg.dct16a_set_option(pkg.OPT_UNIFORM_QUANT, request.param)
+    yield request.param
+    pkg.dct16a_set_option(pkg.OPT_UNIFORM_QUANT, old)
+
+
+@pytest.mark.parametrize("step", [1, 2, 3, 4, 5, 6, 7, 10, 16, 24, 100, 200, 65535])
+def test_codec_uniform_quantiser_choices(step, uniform_quant):
+    """Both uniform quantisers (and the automatic choice) give the oracle's
+    bytes on 10-bit frames and 8-bit images, ragged shapes, small to huge steps."""
+    f = synth.frames_10bit([40, 41], H=48, W=208, workers=1)
+    _codec_check(f, "uniform", 10, step=step)
+    u8 = synth.batch_u8(range(42, 44), 48, 208)
+    _codec_check(u8, "uniform", 8, step=step)
+
+
 @pytest.mark.parametrize("step", [1, 2, 3, 4, 5, 6, 7, 16, 24, 200, 65535])
 @pytest.mark.parametrize("shape", [(1, 16, 16), (2, 48, 208), (1, 32, 1920)])
 def test_codec_uniform_steps_and_shapes(step, shape, codec_path):
@@ -643,7 +663,7 @@ def test_forward_every_store_mode(mode):
 
 
 @pytest.mark.parametrize("step", [2, 4, 6, 8, 24, 40, 72])
-def test_codec_uniform_reconstruction_ties(step, codec_path):
+def test_codec_uniform_reconstruction_ties(step, codec_path, uniform_quant):
     """Flat blocks: only the DC level survives, A′ = Δ·q00/16, an exact .5 tie
     whenever Δ·q00 ≡ 8 (mod 16) — the fused kernel must send those pixels to
     the exact decision (round half away from zero)."""
