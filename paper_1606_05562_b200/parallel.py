@@ -94,6 +94,79 @@ class FusedSseAllReduce:
         return self.buf
 
 
+class IpcSseAllReduce:
+    """The fused in-kernel SSE all-reduce (dct16a_codec_allreduce, peer atomics)
+    over CUDA IPC instead of symmetric memory: every rank cudaMallocs its int64
+    [n_total] vector, the IPC handles are exchanged over the process group, and
+    each rank maps every other rank's vector — which also works for several
+    processes sharing one GPU (symmetric memory refuses that), so the
+    multi-peer path runs on this pool's single-GPU boxes.  Barriers of the
+    process group (after a device synchronisation) order the zeroing before,
+    and the reads after, every rank's kernel."""
+
+    def __init__(self, n_total: int, device, group=None):
+        import torch
+        import torch.distributed as dist
+        from cuda.bindings import runtime as rt
+        self.rt, self.dist, self.group = rt, dist, group
+        self.n_total = int(n_total)
+        self.device = torch.device(device)
+        self.nbytes = 8 * self.n_total
+        err, ptr = rt.cudaMalloc(max(self.nbytes, 8))
+        if err != rt.cudaError_t.cudaSuccess:
+            raise RuntimeError(f"cudaMalloc: {err}")
+        self.ptr = int(ptr)
+        err, h = rt.cudaIpcGetMemHandle(self.ptr)
+        if err != rt.cudaError_t.cudaSuccess:
+            raise RuntimeError(f"cudaIpcGetMemHandle: {err}")
+        handles = [None] * dist.get_world_size(group)
+        dist.all_gather_object(handles, bytes(h.reserved), group=group)
+        me = dist.get_rank(group)
+        self.opened = []
+        self.peers = []
+        for r, hb in enumerate(handles):
+            if r == me:
+                self.peers.append(self.ptr)
+                continue
+            ph = rt.cudaIpcMemHandle_t()
+            ph.reserved = hb
+            err, pp = rt.cudaIpcOpenMemHandle(ph, rt.cudaIpcMemLazyEnablePeerAccess)
+            if err != rt.cudaError_t.cudaSuccess:
+                raise RuntimeError(f"cudaIpcOpenMemHandle (rank {r}): {err}")
+            self.opened.append(int(pp))
+            self.peers.append(int(pp))
+        if len(self.peers) > 8:
+            raise ValueError("dct16a_codec_allreduce supports up to 8 peers")
+
+    def run(self, frames, quant, frame_offset: int, recon=None, desc=None, stream=None):
+        """Codec of this rank's frames; returns the all-reduced per-frame SSE
+        (int64 [n_total], a copy of this rank's vector)."""
+        import torch
+        from . import _lib
+        n = 0 if frames is None else int(frames.shape[0])
+        if frame_offset < 0 or frame_offset + n > self.n_total:
+            raise ValueError(f"frames [{frame_offset}, {frame_offset + n}) outside the vector [0, {self.n_total})")
+        rt = self.rt
+        rt.cudaMemset(self.ptr, 0, self.nbytes)
+        torch.cuda.synchronize(self.device)
+        self.dist.barrier(group=self.group)       # every rank's vector is zero before any kernel adds
+        if n > 0:
+            _lib.dct16a_codec_allreduce(frames, quant, self.peers, frame_offset, recon, desc, stream)
+        torch.cuda.synchronize(self.device)
+        self.dist.barrier(group=self.group)       # every rank's kernel has finished adding
+        out = torch.empty(self.n_total, dtype=torch.int64, device=self.device)
+        rt.cudaMemcpy(out.data_ptr(), self.ptr, self.nbytes, rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice)
+        return out
+
+    def close(self):
+        for pp in self.opened:
+            self.rt.cudaIpcCloseMemHandle(pp)
+        self.opened = []
+        if self.ptr:
+            self.rt.cudaFree(self.ptr)
+            self.ptr = 0
+
+
 def codec_sharded(local_frames, offset: int, n_total: int, mode: str = "uniform", r: int = 16,
                   step: int = 16, valid_height: int | None = None, group=None, want_recon: bool = False):
     """Run the fused codec on this rank's frames and all-reduce the SSE.

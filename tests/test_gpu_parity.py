@@ -974,6 +974,27 @@ def test_config4_sharded_world_gloo_one_gpu(world):
     assert abs(line["global_psnr_db"] - oc.psnr_from_sse(sum(ref["sse"]), 7 * 64 * 208, 10)) < 1e-9
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_allreduce_ipc_several_processes_one_gpu(world):
+    """f2's peer-atomic form across processes: `world` ranks share cuda:0, map
+    each other's SSE vectors through CUDA IPC (parallel.IpcSseAllReduce) and
+    each rank's kernel adds every one of its frames' SSE into all ranks'
+    vectors; every rank's vector equals the gloo all-reduce and the oracle."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={29570 + world}", os.path.join(root, "tools", "run_config4.py"),
+           "--frames", "7", "--height", "64", "--width", "208", "--reps", "1", "--dump", "--backend", "gloo", "--ipc"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["ipc_allreduce"] == {"equal_to_collective": True, "n_peers": world}
+    ref = oc.codec_images(synth.frames_10bit(range(7), H=64, W=208, workers=1), "uniform", step=16, bit_depth=10)
+    assert line["sse"] == ref["sse"]
+
+
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="the fused NVLink/NVLS all-reduce needs >= 2 GPUs")
 def test_fused_allreduce_multi_gpu_equals_nccl():
     """f2 on >= 2 GPUs: the in-kernel all-reduce (multimem.red on the NVLS

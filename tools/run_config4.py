@@ -38,6 +38,9 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--dump", action="store_true", help="print the per-frame SSE vector")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--ipc", action="store_true",
+                    help="fuse the SSE all-reduce into the kernel over CUDA IPC-mapped peer vectors "
+                         "(parallel.IpcSseAllReduce; works with several ranks on one GPU) and check it against NCCL/gloo")
     ap.add_argument("--fused", action="store_true",
                     help="fuse the SSE all-reduce into the kernel (dct16a_codec_allreduce over symmetric memory) "
                          "and check it against the NCCL path")
@@ -49,7 +52,7 @@ def main():
     local = local % torch.cuda.device_count()     # ranks share GPUs when there are fewer GPUs than ranks
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1 or a.fused:
+    if world > 1 or a.fused or a.ipc:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29561")
         if a.backend == "nccl":
@@ -105,6 +108,16 @@ def main():
             f_e1.synchronize()
             fused = {"ms": f_e0.elapsed_time(f_e1) / a.reps, "equal_to_nccl": bool(torch.equal(got, full)),
                      "n_peers": len(fz.targets), "multicast": fz.multicast}
+    ipc = None
+    if a.ipc:
+        iz = parallel.IpcSseAllReduce(a.frames, dev)
+        got = iz.run(x if n else None, q, f0, None, d, stream)
+        got = iz.run(x if n else None, q, f0, None, d, stream)   # twice: zeroing between runs
+        ok = torch.tensor([1 if torch.equal(got, full) else 0], dtype=torch.int32)
+        if world > 1:
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)      # every rank's vector, not only rank 0's
+        ipc = {"equal_to_collective": bool(ok.item()), "n_peers": len(iz.peers)}
+        iz.close()
     if world > 1:
         if a.backend == "gloo":
             ms, ar_ms = ms.cpu(), ar_ms.cpu()
@@ -124,6 +137,8 @@ def main():
                 "pixels": P}
         if fused is not None:
             line["fused_allreduce"] = fused
+        if ipc is not None:
+            line["ipc_allreduce"] = ipc
         if a.dump:
             line["sse"] = full.cpu().tolist()
             line["psnr"] = psnr_frames.cpu().tolist()
