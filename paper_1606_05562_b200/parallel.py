@@ -158,7 +158,16 @@ class IpcSseAllReduce:
         rt.cudaMemcpy(out.data_ptr(), self.ptr, self.nbytes, rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice)
         return out
 
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
     def close(self):
+        """Unmap the peers' vectors and free this rank's (every rank must call it,
+        after the last run(); also on leaving a `with` block)."""
         for pp in self.opened:
             self.rt.cudaIpcCloseMemHandle(pp)
         self.opened = []

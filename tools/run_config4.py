@@ -110,14 +110,14 @@ def main():
                      "n_peers": len(fz.targets), "multicast": fz.multicast}
     ipc = None
     if a.ipc:
-        iz = parallel.IpcSseAllReduce(a.frames, dev)
-        got = iz.run(x if n else None, q, f0, None, d, stream)
-        got = iz.run(x if n else None, q, f0, None, d, stream)   # twice: zeroing between runs
+        with parallel.IpcSseAllReduce(a.frames, dev) as iz:
+            got = iz.run(x if n else None, q, f0, None, d, stream)
+            got = iz.run(x if n else None, q, f0, None, d, stream)   # twice: zeroing between runs
+            n_peers = len(iz.peers)
         ok = torch.tensor([1 if torch.equal(got, full) else 0], dtype=torch.int32)
         if world > 1:
             dist.all_reduce(ok, op=dist.ReduceOp.MIN)      # every rank's vector, not only rank 0's
-        ipc = {"equal_to_collective": bool(ok.item()), "n_peers": len(iz.peers)}
-        iz.close()
+        ipc = {"equal_to_collective": bool(ok.item()), "n_peers": n_peers}
     if world > 1:
         if a.backend == "gloo":
             ms, ar_ms = ms.cpu(), ar_ms.cpu()
