@@ -171,6 +171,8 @@ class IpcSseAllReduce:
         for pp in self.opened:
             self.rt.cudaIpcCloseMemHandle(pp)
         self.opened = []
+        if self.ptr and self.dist.is_initialized():
+            self.dist.barrier(group=self.group)   # no rank still maps this vector
         if self.ptr:
             self.rt.cudaFree(self.ptr)
             self.ptr = 0
