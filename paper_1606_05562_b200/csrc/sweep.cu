@@ -59,8 +59,12 @@ __constant__ ZZTable c_zz = make_zz();
 template <int ELEM>
 struct SCfg {
     static constexpr int kStageBytes = 16 * kWTile * 16 * ELEM;
-    // per warp: stages | Y transposition (2 x 336 floats) + W⊙Z (2 x 257 floats) | SSE[256] u64
-    static constexpr int kYBytes = 3072, kZBytes = 2048, kSseBytes = 2048;
+    // rows per lane in the sweep: every lane carries row t of two blocks, so each step's
+    // operands (zig-zag cell, T_ki, the row T_l) are fetched once for both (config 5:
+    // 2.32 -> 2.00 ms; 10-bit 0.96 -> 0.87 ms)
+    static constexpr int kRPL = 2;
+    // per warp: stages | Y transposition (2 x 336 floats) + W⊙Z (2·kRPL x 257 floats) | SSE[256] u64
+    static constexpr int kYBytes = 3072, kZBytes = 2048 * kRPL, kSseBytes = 2048;
     static constexpr int kWarpBytes = kSStages * kStageBytes + kYBytes + kZBytes + kSseBytes;
     static_assert(kWarpBytes % 1024 == 0, "stages must stay 1024-byte aligned");
     static constexpr int kTBytes = 1024;   // T as floats, shared by the CTA
@@ -157,118 +161,141 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
         }
         const int nb = min(kWTile, p.BX - x0 / 16);
         const bool row_valid = by * 16 + t < p.VH;
+        constexpr int RPL = Cfg::kRPL;
 #pragma unroll 1
-        for (int pair = 0; 2 * pair < nb; ++pair) {
-            const int bb = 2 * pair + h;
-            const bool contributes = bb < nb && row_valid;
-            int a0, a1;
-            row_addr<ELEM>(bb, t, &a0, &a1);
-            float xs[16];          // 10-bit: 2^23 + x[i][j], the SSE reference in the magic-float domain
-            uint32_t xw[4];        // 8-bit: the packed original row (vabsdiff4/dp4a reference)
-            {
-                uint32_t w[4 * ELEM];
-                load_px<ELEM>(stage, a0, a1, w);
-                if (ELEM == 1) {
+        for (int grp = 0; 2 * RPL * grp < nb; ++grp) {
+            // lane (h, t): row t of blocks 2·RPL·grp + 2u + h, u < RPL
+            bool contributes[RPL];
+            float xs[RPL][ELEM == 2 ? 16 : 1];   // 10-bit: 2^23 + x[i][j], the SSE reference in the magic-float domain
+            uint32_t xw[RPL][4];                 // 8-bit: the packed original row (vabsdiff4/dp4a reference)
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) xw[q] = w[q];
+            for (int u = 0; u < RPL; ++u) {
+                const int bb = 2 * RPL * grp + 2 * u + h;
+                contributes[u] = bb < nb && row_valid;
+                int a0, a1;
+                row_addr<ELEM>(bb, t, &a0, &a1);
+                {
+                    uint32_t w[4 * ELEM];
+                    load_px<ELEM>(stage, a0, a1, w);
+                    if (ELEM == 1) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) xw[u][q] = w[q];
+                    }
+                    float x[16], y[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        x[j] = px_float<ELEM>(w, j);
+                        if constexpr (ELEM == 2) xs[u][j] = 8388608.0f + x[j];
+                    }
+                    net_fwd(x, y);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        *reinterpret_cast<float4*>(ty + t * 20 + 4 * q) = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
                 }
-                float x[16], y[16];
+                __syncwarp();
+                {
+                    float col[16], z[16];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    x[j] = px_float<ELEM>(w, j);
-                    xs[j] = 8388608.0f + x[j];
+                    for (int k = 0; k < 16; ++k) col[k] = ty[k * 20 + l];
+                    net_fwd(col, z);
+                    float* wzu = wz + u * 2 * 257;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k)
+                        wzu[k * 16 + l] = z[k] * (g_of(k) == 16 ? w16 : (g_of(k) == 12 ? w12 : w8));
                 }
-                net_fwd(x, y);
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    *reinterpret_cast<float4*>(ty + t * 20 + 4 * q) = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+                __syncwarp();
             }
-            __syncwarp();
-            {
-                float col[16], z[16];
+            // ---- the sweep, lane = row i = t of each of its RPL blocks
+            // N[u][i][2m], N[u][i][2m+1] as one float2: the update and the rounding are FFMA2
+            float2 N[RPL][8];
 #pragma unroll
-                for (int k = 0; k < 16; ++k) col[k] = ty[k * 20 + l];
-                net_fwd(col, z);
+            for (int u = 0; u < RPL; ++u)
 #pragma unroll
-                for (int k = 0; k < 16; ++k)
-                    wz[k * 16 + l] = z[k] * (g_of(k) == 16 ? w16 : (g_of(k) == 12 ? w12 : w8));
-            }
-            __syncwarp();
-            // ---- the sweep, lane = row i = t
-            // N[i][2m], N[i][2m+1] as one float2: the update and the rounding are FFMA2
-            float2 N[8];
-#pragma unroll
-            for (int m = 0; m < 8; ++m) N[m] = make_float2(1152.5f * 0x1p-35f, 1152.5f * 0x1p-35f);
-            // operands of the rank-1 step r (zig-zag cell of rank r-1), prefetched one step ahead
-            float sv;
+                for (int m = 0; m < 8; ++m) N[u][m] = make_float2(1152.5f * 0x1p-35f, 1152.5f * 0x1p-35f);
+            // operands of the rank-1 step r (zig-zag cell of rank r-1), prefetched one step ahead:
+            // W⊙Z_kl·T_ki of each block (T_ki shared: row i = t of every block) and the row T_l
+            float sv[RPL];
             float4 tq[4];
-            auto fetch = [&](int r, float& s_out, float4 (&t_out)[4]) {
+            auto fetch = [&](int r, float (&s_out)[RPL], float4 (&t_out)[4]) {
                 const int kl = c_zz.v[min(r, 256) - 1];
-                s_out = wz[kl] * Ts[(kl >> 4) * 16 + t];
+                const float tk = Ts[(kl >> 4) * 16 + t];
+#pragma unroll
+                for (int u = 0; u < RPL; ++u) s_out[u] = wz[u * 2 * 257 + kl] * tk;
                 const float4* tr = reinterpret_cast<const float4*>(Ts + (kl & 15) * 16);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) t_out[q] = tr[q];
             };
             auto update = [&]() {
-                const float2 s2 = make_float2(sv, sv);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    N[2 * q] = __ffma2_rn(s2, make_float2(tq[q].x, tq[q].y), N[2 * q]);
-                    N[2 * q + 1] = __ffma2_rn(s2, make_float2(tq[q].z, tq[q].w), N[2 * q + 1]);
+                for (int u = 0; u < RPL; ++u) {
+                    const float2 s2 = make_float2(sv[u], sv[u]);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        N[u][2 * q] = __ffma2_rn(s2, make_float2(tq[q].x, tq[q].y), N[u][2 * q]);
+                        N[u][2 * q + 1] = __ffma2_rn(s2, make_float2(tq[q].z, tq[q].w), N[u][2 * q + 1]);
+                    }
                 }
+            };
+            auto rotate = [&](const float (&svn)[RPL], const float4 (&tqn)[4]) {
+#pragma unroll
+                for (int u = 0; u < RPL; ++u) sv[u] = svn[u];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) tq[q] = tqn[q];
             };
             const float2 inv2 = make_float2(inv2304, inv2304), m2 = make_float2(8388608.0f, 8388608.0f);
             const float2 pix2 = make_float2(0x1p-114f / 2304.0f, 0x1p-114f / 2304.0f);
             fetch(1, sv, tq);
 #pragma unroll 1
             for (int r = 1; r < p.r_first; ++r) {   // below the requested range: update only
-                float svn;
+                float svn[RPL];
                 float4 tqn[4];
                 fetch(r + 1, svn, tqn);
                 update();
-                sv = svn;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) tq[q] = tqn[q];
+                rotate(svn, tqn);
             }
 #pragma unroll kSweepUnroll
             for (int r = p.r_first; r <= p.r_last; ++r) {
-                float svn;
+                float svn[RPL];
                 float4 tqn[4];
                 fetch(r + 1, svn, tqn);
                 update();
-                unsigned ei;
-                if (ELEM == 1) {
-                    // floor((N + 1152.5)/2304) by one round-down FMA onto 2^23 (exact, see
-                    // header); cvt.pack.sat clamps to [0, 255] and packs 4 pixels, then
-                    // vabsdiff4 + dp4a square and sum against the original bytes
-                    ei = 0;
+                unsigned ei = 0;
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        // (N·2^-35)·fl(2^-114/2304) rounded down to the subnormal grid:
-                        // the bits are floor(N·fl(1/2304)) (negative -> sign bit -> 0)
-                        const float2 f0 = fmul2_rd_keep_subnormal(N[2 * q], pix2), f1 = fmul2_rd_keep_subnormal(N[2 * q + 1], pix2);
-                        const int v[4] = {__float_as_int(f0.x), __float_as_int(f0.y), __float_as_int(f1.x),
-                                          __float_as_int(f1.y)};
-                        const uint32_t pk = pack2_sat_u8(v[1], v[0], pack2_sat_u8(v[3], v[2], 0u));
-                        const uint32_t d = __vabsdiffu4(pk, xw[q]);
-                        ei = __dp4a(d, d, ei);
-                    }
-                } else {
-                    float2 e2 = make_float2(0.0f, 0.0f);
+                for (int u = 0; u < RPL; ++u) {
+                    unsigned eu;
+                    if (ELEM == 1) {
+                        // (N·2^-35)·fl(2^-114/2304) rounded down to the subnormal grid: the bits
+                        // are floor(N·fl(1/2304)) (negative -> sign bit -> 0); cvt.pack.sat clamps
+                        // to [0, 255] and packs 4 pixels, vabsdiff4 + dp4a square and sum
+                        eu = 0;
 #pragma unroll
-                    for (int m = 0; m < 8; ++m) {
-                        const float2 f = __ffma2_rd(N[m], inv2, m2);
-                        const float2 fc = make_float2(fminf(fmaxf(f.x, 8388608.0f), top), fminf(fmaxf(f.y, 8388608.0f), top));
-                        const float2 d = __fadd2_rn(fc, make_float2(-xs[2 * m], -xs[2 * m + 1]));
-                        e2 = __ffma2_rn(d, d, e2);
+                        for (int q = 0; q < 4; ++q) {
+                            const float2 f0 = fmul2_rd_keep_subnormal(N[u][2 * q], pix2),
+                                         f1 = fmul2_rd_keep_subnormal(N[u][2 * q + 1], pix2);
+                            const int v[4] = {__float_as_int(f0.x), __float_as_int(f0.y), __float_as_int(f1.x),
+                                              __float_as_int(f1.y)};
+                            const uint32_t pk = pack2_sat_u8(v[1], v[0], pack2_sat_u8(v[3], v[2], 0u));
+                            const uint32_t d = __vabsdiffu4(pk, xw[u][q]);
+                            eu = __dp4a(d, d, eu);
+                        }
+                    } else {
+                        // floor((N + 1152.5)/2304) by one round-down FMA onto 2^23 (exact, header),
+                        // float32 clamp and squared error (exact below 2^24 per row)
+                        float2 e2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) {
+                            const float2 f = __ffma2_rd(N[u][m], inv2, m2);
+                            const float2 fc = make_float2(fminf(fmaxf(f.x, 8388608.0f), top), fminf(fmaxf(f.y, 8388608.0f), top));
+                            const float2 d = __fadd2_rn(fc, make_float2(-xs[u][2 * m], -xs[u][2 * m + 1]));
+                            e2 = __ffma2_rn(d, d, e2);
+                        }
+                        eu = __float2uint_rn(e2.x + e2.y);
                     }
-                    ei = __float2uint_rn(e2.x + e2.y);
+                    ei += contributes[u] ? eu : 0u;
                 }
-                const unsigned tot = __reduce_add_sync(0xffffffffu, contributes ? ei : 0u);
+                const unsigned tot = __reduce_add_sync(0xffffffffu, ei);
                 if (lane == 0) ssew[r - p.r_first] += tot;   // this warp's own accumulator: no atomic
-                sv = svn;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) tq[q] = tqn[q];
+                rotate(svn, tqn);
             }
             __syncwarp();
         }
