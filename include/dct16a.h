@@ -281,8 +281,9 @@ DCT16A_API int64_t dct16a_forward_host_workspace(const dct16a_desc* desc, int32_
  * same bytes).  Initial values come from the environment variables named
  * below; set_option returns DCT16A_EDOMAIN for an unknown option or value.
  *   DCT16A_OPT_CODEC_PATH (env DCT16A_CODEC_PATH): fused-codec kernel choice,
- *     0 = automatic (default): zonal 8-bit with r <= 36 on the band-pruned
- *         warp-per-tile kernel, everything else on the warp-per-block-pair kernel;
+ *     0 = automatic (default): every zonal case on the band-pruned
+ *         warp-per-tile kernel (8- and 10-bit, any r), uniform on the
+ *         warp-per-block-pair kernel;
  *     2 = always the warp-per-block-pair kernel.
  *     (Libraries built with -DDCT16A_EXPERIMENTS also take 1 = zonal on the
  *     generic kernel and 3 = zonal 8-bit r <= 36 on the thread-per-block kernel.)

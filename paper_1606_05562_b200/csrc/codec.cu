@@ -522,8 +522,8 @@ int launch_codec_generic(const void* src, const Geom& g, const dct16a_quant& q, 
 #endif  // DCT16A_EXPERIMENTS
 
 // Kernel choice of the fused codec (option DCT16A_OPT_CODEC_PATH, include/dct16a.h):
-//   0 auto: zonal 8-bit with r <= 36 -> band-pruned warp kernel (zonal_band.cu),
-//           everything else -> warp-per-block-pair kernel (codec_warp.cu);
+//   0 auto: zonal (8/10-bit, every r) -> band-pruned warp-per-tile kernel
+//           (zonal_band.cu), uniform -> warp-per-block-pair kernel (codec_warp.cu);
 //   2: always codec_warp.cu.
 // Experiment builds (-DDCT16A_EXPERIMENTS) add 1 (zonal on the generic kernel
 // above), 3 (zonal 8-bit r <= 36 on the thread-per-block kernel, zonal_tpb.cu)
@@ -538,7 +538,7 @@ int launch_codec(const void* src, const Geom& g, const dct16a_quant& q, void* re
     int rc;
     if (zonal && path == 0 && zonal_band_applies(g, q.r)) rc = launch_zonal_band(src, g, q.r, recon, sse, st);
 #ifdef DCT16A_EXPERIMENTS
-    else if (zonal && path == 3 && zonal_band_applies(g, q.r)) rc = launch_zonal_tpb(src, g, q.r, recon, sse, st);
+    else if (zonal && path == 3 && g.elem == 1 && zonal_band(q.r) <= 7) rc = launch_zonal_tpb(src, g, q.r, recon, sse, st);
     else if (zonal && path == 1) rc = launch_codec_generic(src, g, q, recon, sse, st);
 #endif
 #ifdef DCT16A_EXPERIMENTS

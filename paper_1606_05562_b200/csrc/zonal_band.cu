@@ -1,6 +1,6 @@
 // zonal_band.cu — fused zonal codec, warp-cooperative and band-pruned, for
-// 8- and 10-bit images and r <= 136 (configs 1, 3; the zonal r-sweep's single
-// points): forward -> keep the first r zig-zag
+// 8- and 10-bit images and every r (configs 1, 3; the zonal r-sweep's single
+// points; r > 136 runs the unpruned BAND = 15 instance): forward -> keep the first r zig-zag
 // coefficients with S folded into the weights ->
 // inverse (896-901) -> round half away / clamp (reading A6) -> per-image SSE
 // (906-910).
@@ -477,7 +477,7 @@ int launch_zb_e(const void* src, const Geom& g, int r, void* recon, uint64_t* ss
     if (band <= 5) return launch_zb<ELEM, 5>(src, g, r, recon, sse, st);
     if (band <= 7) return launch_zb<ELEM, 7>(src, g, r, recon, sse, st);
     if (band <= 11) return launch_zb<ELEM, 11>(src, g, r, recon, sse, st);
-    return launch_zb<ELEM, 15>(src, g, r, recon, sse, st);
+    return launch_zb<ELEM, 15>(src, g, r, recon, sse, st);   // also every r > 136 (band > 15)
 }
 
 }  // namespace
@@ -489,13 +489,15 @@ int zonal_band(int r) {
     return d;
 }
 
-// The band kernel covers every r whose zig-zag prefix lies in k + l <= 15
-// (r <= 136), 8- and 10-bit; beyond, no output of the forward can be pruned.
-bool zonal_band_applies(const Geom& g, int r) { (void)g; return zonal_band(r) <= 15; }
+// The band kernel covers every r, 8- and 10-bit: r <= 136 on the smallest band
+// k + l <= BAND holding the zig-zag prefix; beyond (k + l reaching 16..30) on
+// BAND = 15, which computes every output of both networks (nothing left to
+// prune) and keeps the first r cells through the weights (zero elsewhere).
+bool zonal_band_applies(const Geom& g, int r) { (void)g; return r >= 1 && r <= 256; }
 
 // Callers check zonal_band_applies first.
 int launch_zonal_band(const void* src, const Geom& g, int r, void* recon, uint64_t* sse, cudaStream_t st) {
-    if (zonal_band(r) > 15) return DCT16A_EDOMAIN;
+    if (r < 1 || r > 256) return DCT16A_EDOMAIN;
     return g.elem == 1 ? launch_zb_e<1>(src, g, r, recon, sse, st) : launch_zb_e<2>(src, g, r, recon, sse, st);
 }
 

@@ -294,7 +294,7 @@ int launch_ztpb(const void* src, const Geom& g, int r, void* recon, uint64_t* ss
 
 }  // namespace
 
-// Callers check zonal_band_applies first (8-bit, r <= 36).
+// Callers check that it applies first (8-bit, r <= 36).
 int launch_zonal_tpb(const void* src, const Geom& g, int r, void* recon, uint64_t* sse, cudaStream_t st) {
     const int band = zonal_band(r);
     if (g.elem != 1 || band > 7) return DCT16A_EDOMAIN;

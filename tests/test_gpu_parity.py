@@ -195,7 +195,7 @@ def test_psnr_kernel():
 def codec_path(request):
     """Every fused-codec test runs on each kernel choice of the product build
     (DCT16A_OPT_CODEC_PATH): the automatic choice (band-pruned warp-per-tile
-    kernel for 8-bit zonal r <= 36) and the warp-per-block-pair kernel for
+    kernel for every zonal case) and the warp-per-block-pair kernel for
     everything, each checked against the oracle independently."""
     old = pkg.dct16a_get_option(pkg.OPT_CODEC_PATH)
     pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, request.param)
@@ -221,7 +221,7 @@ def test_codec_config1(codec_path):
 
 @pytest.mark.parametrize("r", [1, 2, 10, 11, 16, 21, 22, 32, 36, 37, 100, 256])
 def test_codec_zonal_varied(r, codec_path):
-    # r <= 36 runs the band-pruned kernels (bands 3/5/7), larger r the warp-per-block-pair one
+    # automatic choice: the band kernel on the smallest band holding r (r > 136: band 15, unpruned)
     imgs = np.concatenate([synth.batch_u8([40, 41], 48, 272), synth.adversarial_u8(48, 272)])
     _codec_check(imgs, "zonal", 8, r=r)
 
@@ -1017,11 +1017,12 @@ def test_fused_allreduce_multi_gpu_equals_nccl():
 
 
 @pytest.mark.parametrize("bd", [8, 10])
-def test_band_kernel_every_r_up_to_136(bd):
-    """The band-pruned zonal kernel (codec path 0) for every r it serves,
-    1..136 (bands 3/5/7/11/15; one or two columns per lane), 8- and 10-bit,
-    on a ragged strip (17 blocks: a partial tile) with pitched rows: pixels
-    and SSE equal the oracle, and the warp kernel (path 2) byte for byte."""
+def test_band_kernel_every_r(bd):
+    """The band-pruned zonal kernel (codec path 0) for every r, 1..256 (bands
+    3/5/7/11/15; one or two columns per lane; r > 136 on the unpruned band 15),
+    8- and 10-bit, on a ragged strip (17 blocks: a partial tile) with pitched
+    rows: pixels and SSE equal the oracle, and the warp kernel (path 2) byte
+    for byte."""
     hi = 256 if bd == 8 else 1024
     rng = np.random.default_rng(77 + bd)
     if bd == 8:
@@ -1035,14 +1036,14 @@ def test_band_kernel_every_r_up_to_136(bd):
     t = to_dev(base)[:, :, :272]
     old = pkg.dct16a_get_option(pkg.OPT_CODEC_PATH)
     try:
-        for r in range(1, 137):
+        for r in range(1, 257):
             pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, 0)
             rec, sse, _ = pkg.codec(t, "zonal", r=r)
             pkg.dct16a_set_option(pkg.OPT_CODEC_PATH, 2)
             rec2, sse2, _ = pkg.codec(t, "zonal", r=r)
             torch.cuda.synchronize()
             assert torch.equal(rec, rec2) and torch.equal(sse, sse2), r
-            if r in (1, 2, 6, 7, 10, 15, 16, 21, 28, 29, 36, 37, 45, 64, 66, 78, 79, 100, 120, 136):
+            if r in (1, 2, 6, 7, 10, 15, 16, 21, 28, 29, 36, 37, 45, 64, 66, 78, 79, 100, 120, 136, 137, 150, 200, 255, 256):
                 ref = oc.codec_images(vc, "zonal", r=r, bit_depth=bd)
                 assert np.array_equal(rec.cpu().numpy(), ref["recon_img"]), r
                 assert sse.cpu().tolist() == ref["sse"], r
