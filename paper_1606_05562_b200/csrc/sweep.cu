@@ -42,7 +42,6 @@ namespace {
 #endif
 constexpr int kSweepUnroll = DCT16A_SWEEP_UNROLL;   // measured r-loop unroll
 constexpr int kSWarps = 4;    // warps per CTA
-constexpr int kSStages = 3;   // TMA ring depth per warp
 
 // zig-zag order as a table: kZZ[r] = 16·k + l of the cell with rank r (reading A4)
 struct ZZTable {
@@ -58,6 +57,10 @@ __constant__ ZZTable c_zz = make_zz();
 
 template <int ELEM>
 struct SCfg {
+    // TMA ring depth per warp: every tile is 256 rank-1 steps of work, so two stages
+    // hide the loads for 8-bit input and free the shared memory for a fourth CTA
+    // (16 warps/SM: config 5 2.00 -> 1.97 ms); 10-bit keeps three (0.87 against 0.93 ms)
+    static constexpr int kSStages = ELEM == 1 ? 2 : 3;
     static constexpr int kStageBytes = 16 * kWTile * 16 * ELEM;
     // rows per lane in the sweep: every lane carries row t of two blocks, so each step's
     // operands (zig-zag cell, T_ki, the row T_l) are fetched once for both (config 5:
@@ -91,14 +94,14 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
     const int lane = threadIdx.x & 31;
     const int h = lane >> 4, t = lane & 15;
     uint8_t* wbase = smem + warp * Cfg::kWarpBytes;
-    float* ty = reinterpret_cast<float*>(wbase + kSStages * Cfg::kStageBytes) + h * (16 * 20 + 16);
+    float* ty = reinterpret_cast<float*>(wbase + Cfg::kSStages * Cfg::kStageBytes) + h * (16 * 20 + 16);
     // W⊙Z of the block pair right after the Y tile (2 x 336 floats); the second block
     // starts 257 floats later so the two half-warps' broadcasts hit different banks
-    float* wz = reinterpret_cast<float*>(wbase + kSStages * Cfg::kStageBytes) + 2 * 336 + h * 257;
+    float* wz = reinterpret_cast<float*>(wbase + Cfg::kSStages * Cfg::kStageBytes) + 2 * 336 + h * 257;
     unsigned long long* ssew =
-        reinterpret_cast<unsigned long long*>(wbase + kSStages * Cfg::kStageBytes + Cfg::kYBytes + Cfg::kZBytes);
+        reinterpret_cast<unsigned long long*>(wbase + Cfg::kSStages * Cfg::kStageBytes + Cfg::kYBytes + Cfg::kZBytes);
     float* Ts = reinterpret_cast<float*>(smem + kSWarps * Cfg::kWarpBytes);   // Ts[k*16 + i] = T[k][i]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSWarps * Cfg::kWarpBytes + Cfg::kTBytes) + warp * kSStages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSWarps * Cfg::kWarpBytes + Cfg::kTBytes) + warp * Cfg::kSStages;
 
     // T from the network of Eq. (1): column i = net_fwd(e_i)
     if (threadIdx.x < 16) {
@@ -117,12 +120,12 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
     if (t1 > p.n_tiles) t1 = p.n_tiles;
     const uint64_t pol = policy_evict_first();
     if (lane == 0) {
-        for (int s = 0; s < kSStages; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < Cfg::kSStages; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
         prefetch_tmap(&tin);
         TileCursor ic;
         ic.init(p, t0);
-        for (int s = 0; s < kSStages - 1; ++s) {
+        for (int s = 0; s < Cfg::kSStages - 1; ++s) {
             if (t0 + s < t1) w_issue_at<ELEM>(&tin, p, ic, wbase + s * Cfg::kStageBytes, &bars[s], pol);
             ic.advance(p);
         }
@@ -143,11 +146,11 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
     int it = 0;
     TileCursor cc, nc;   // the tile being consumed and the one kSStages - 1 ahead (next to issue)
     cc.init(p, t0);
-    nc.init(p, t0 + kSStages - 1);
+    nc.init(p, t0 + Cfg::kSStages - 1);
     for (long long tix = t0; tix < t1; ++tix, ++it, cc.advance(p), nc.advance(p)) {
-        const int s = it % kSStages;
+        const int s = it % Cfg::kSStages;
         uint8_t* stage = wbase + s * Cfg::kStageBytes;
-        mbar_wait(&bars[s], (it / kSStages) & 1);
+        mbar_wait(&bars[s], (it / Cfg::kSStages) & 1);
         const int n = cc.n, by = cc.by, x0 = cc.x0();
         if (n != cur_n) {   // flush the per-r SSE of the previous image (warp-uniform)
             __syncwarp();
@@ -300,9 +303,9 @@ __global__ void __launch_bounds__(kSWarps * 32, SCfg<ELEM>::kCtasPerSm)
             __syncwarp();
         }
         if (lane == 0) {
-            const long long nt = tix + kSStages - 1;
-            if (nt < t1) w_issue_at<ELEM>(&tin, p, nc, wbase + ((it + kSStages - 1) % kSStages) * Cfg::kStageBytes,
-                                       &bars[(it + kSStages - 1) % kSStages], pol);
+            const long long nt = tix + Cfg::kSStages - 1;
+            if (nt < t1) w_issue_at<ELEM>(&tin, p, nc, wbase + ((it + Cfg::kSStages - 1) % Cfg::kSStages) * Cfg::kStageBytes,
+                                       &bars[(it + Cfg::kSStages - 1) % Cfg::kSStages], pol);
         }
         __syncwarp();
     }
