@@ -58,14 +58,15 @@ __constant__ ZZTable c_zz = make_zz();
 template <int ELEM>
 struct SCfg {
     // TMA ring depth per warp: every tile is 256 rank-1 steps of work, so two stages
-    // hide the loads for 8-bit input and free the shared memory for a fourth CTA
-    // (16 warps/SM: config 5 2.00 -> 1.97 ms); 10-bit keeps three (0.87 against 0.93 ms)
+    // hide the loads for 8-bit input (shared memory for 3 CTAs with four rows per lane);
+    // 10-bit keeps three (0.87 against 0.93 ms)
     static constexpr int kSStages = ELEM == 1 ? 2 : 3;
     static constexpr int kStageBytes = 16 * kWTile * 16 * ELEM;
-    // rows per lane in the sweep: every lane carries row t of two blocks, so each step's
-    // operands (zig-zag cell, T_ki, the row T_l) are fetched once for both (config 5:
-    // 2.32 -> 2.00 ms; 10-bit 0.96 -> 0.87 ms)
-    static constexpr int kRPL = 2;
+    // rows per lane in the sweep: every lane carries row t of several blocks (four for
+    // 8-bit input: the whole 8-block tile; two for 10-bit), so each step's operands
+    // (zig-zag cell, T_ki, the row T_l) are fetched once for all of them (config 5:
+    // 2.32 ms with one row, 2.00 with two, 1.86 with four; 10-bit 0.96 -> 0.87 ms with two)
+    static constexpr int kRPL = ELEM == 1 ? 4 : 2;
     // per warp: stages | Y transposition (2 x 336 floats) + W⊙Z (2·kRPL x 257 floats) | SSE[256] u64
     static constexpr int kYBytes = 3072, kZBytes = 2048 * kRPL, kSseBytes = 2048;
     static constexpr int kWarpBytes = kSStages * kStageBytes + kYBytes + kZBytes + kSseBytes;
