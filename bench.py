@@ -57,7 +57,7 @@ CFG4_DISTINCT = 64
 ISSUE_COUNTS = {
     "cfg3": (641.4 / 8, "profiles/r02_ncu_cfg3_band.txt: 641.4 per 8-block tile, zband_kernel<1,7>"),
     "cfg4": (679.0 / 2, "profiles/r02_ncu_cfg4_final.txt: 550.0e6 per 810,000 block pairs, codec_warp_kernel<2,1>"),
-    "cfg5": (47.5 / 2 * 256, "profiles/r02_ncu_cfg5.txt: 1.594e9 per 131,072 block pairs x 256 r = 47.5 per r per pair, sweep_kernel<1>"),
+    "cfg5": (43.7 / 2 * 256, "profiles/r02_ncu_cfg5.txt: 1.465e9 per 131,072 block pairs x 256 r = 43.7 per r per pair, sweep_kernel<1>"),
 }
 
 
